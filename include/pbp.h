@@ -1,0 +1,180 @@
+/*
+ * pbp.h -- C ABI of the B200 batched polar-code BP decoder (libpbp.so).
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no torch or C++
+ * types. Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj). The C++ mirror of the
+ * reference headers (include/polarbp/*.hpp, namespace polarbp) is
+ * implemented on top of these calls; see INTEGRATION.md for the bindings.
+ *
+ * Conventions
+ *   - Rows are 0-based natural order, as in include/polarbp/bp_core.hpp:6-9.
+ *   - Positive LLR favours bit 0 (include/polarbp/channel.hpp:2-3).
+ *   - Bit vectors are packed little-endian into uint32 words: bit (r % 32)
+ *     of word (r / 32) holds row r; ceil(n/32) words per frame.
+ *   - Decoders compute in fp32 in the reference's fp32 operation order
+ *     (SURVEY.md 8c "ref32"): hard decisions, iteration counts, PE counts,
+ *     stop reasons and freeze-event counts equal the reference compiled in
+ *     fp32 on the same fp32 LLRs.
+ *   - Every call returns PBP_OK (0) or a status; pbp_last_error() gives the
+ *     message (thread-local). The reference throws std::invalid_argument /
+ *     std::runtime_error with the same texts; the C++ wrapper rethrows them.
+ *   - There is no CPU fallback: without a usable CUDA device every decode
+ *     call fails with PBP_ENODEV.
+ */
+#ifndef PBP_H
+#define PBP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PBP_VERSION 1
+
+typedef enum {
+    PBP_OK = 0,
+    PBP_EINVAL = 1,  /* std::invalid_argument in the reference */
+    PBP_ERUNTIME = 2,/* std::runtime_error in the reference     */
+    PBP_ECUDA = 3,   /* CUDA runtime failure                     */
+    PBP_ENODEV = 4,  /* no CUDA device                           */
+    PBP_ENOMEM = 5
+} pbp_status;
+
+/* DecoderKind (include/polarbp/sim_harness.hpp:19) */
+typedef enum { PBP_BASELINE = 0, PBP_GMATRIX = 1, PBP_CSFG = 2 } pbp_decoder;
+/* StopReason (include/polarbp/bp_core.hpp:48) */
+typedef enum { PBP_STOP_MAX_ITER = 0, PBP_STOP_GMATRIX = 1, PBP_STOP_CSFG = 2 } pbp_stop_reason;
+
+/* PolarCode (include/polarbp/polar_code.hpp:27-32): n = 2^m, k info rows,
+ * frozen[r] != 0 marks a frozen row. Host memory, caller-owned. */
+typedef struct {
+    int32_t n;
+    int32_t m;
+    int32_t k;
+    const uint8_t* frozen;
+} pbp_code;
+
+/* One device context: device buffers, stream, cached code tables. Not
+ * thread-safe; use one context per host thread (reference decoders are
+ * pure functions, SPEC: concurrent calls on distinct frames are safe). */
+typedef struct pbp_ctx pbp_ctx;
+
+/* Per-frame outputs of a batch (DecodeOutcome, include/polarbp/bp_core.hpp:51-57
+ * plus the FreezeEvent count of csfg_freeze.hpp:28-35). Any field may be NULL. */
+typedef struct {
+    uint32_t* u_hat_bits; /* frames x ceil(n/32) words */
+    int32_t* iterations;  /* iterations_used           */
+    int64_t* pe;          /* pe_activations            */
+    uint8_t* stop;        /* pbp_stop_reason           */
+    int32_t* n_events;    /* freeze events (csfg)      */
+} pbp_frame_out;
+
+/* Accumulator (src/sim_harness.cpp:56-63) plus event and stop histograms.
+ * Integer sums: identical for any sharding of trials across GPUs. */
+typedef struct {
+    int64_t frames;
+    int64_t bit_errors;
+    int64_t frame_errors;
+    int64_t sum_iters;
+    int64_t sum_iters_sq;
+    int64_t sum_pe;
+    int64_t sum_events;
+    int64_t stop_hist[3];
+} pbp_counters;
+
+const char* pbp_last_error(void);
+int pbp_version(void);
+/* Number of visible CUDA devices (0 on a CPU-only host). */
+int pbp_device_count(void);
+
+int pbp_ctx_create(int device, pbp_ctx** out);
+int pbp_ctx_destroy(pbp_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) for callers that order their own work. */
+void* pbp_ctx_stream(pbp_ctx* ctx);
+int pbp_ctx_synchronize(pbp_ctx* ctx);
+
+/* ---- host-side code helpers (PolarCode::construct, polar_code.cpp:53-66;
+ *      polar_transform_inplace, polar_code.cpp:13-20; encode, :82-91) ---- */
+int pbp_construct(int32_t n, int32_t k, double design_z, uint8_t* frozen_out);
+int pbp_polar_transform(uint8_t* bits, int32_t n);
+int pbp_encode(const pbp_code* code, const uint8_t* info, uint8_t* u_out, uint8_t* x_out);
+/* noise_variance (src/channel.cpp:9-15) */
+int pbp_noise_variance(double ebn0_db, double rate, double* out);
+
+/* ---- decode ------------------------------------------------------------
+ * Replaces decode_baseline / decode_gmatrix (include/polarbp/bp_core.hpp:84-87)
+ * and decode_csfg (include/polarbp/csfg_freeze.hpp:109-111), batched over
+ * `frames` independent frames. llrs: frames x n fp32, row-major.
+ *
+ * pbp_decode_batch: HOST buffers in and out (copies inside the call).
+ * pbp_decode_batch_device: DEVICE pointers, asynchronous on `stream`
+ * (NULL = the context stream); outputs valid after the stream syncs. */
+int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs,
+                     int64_t frames, float alpha, int32_t max_iter, pbp_frame_out* out);
+int pbp_decode_batch_device(pbp_ctx* ctx, const pbp_code* code, int decoder,
+                            const float* llrs_dev, int64_t frames, float alpha,
+                            int32_t max_iter, pbp_frame_out* out_dev, void* stream);
+
+/* Single-frame decode with the freeze-event trace of decode_csfg's
+ * optional `events` out-param (csfg_freeze.hpp:109-111). events receives
+ * 5 int32 per event (iteration 1-based, stage, block, start, size), at most
+ * events_cap events; *n_events is the full count. Host buffers. */
+int pbp_decode_trace(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs,
+                     float alpha, int32_t max_iter, uint8_t* u_hat, int32_t* iterations,
+                     int64_t* pe, int32_t* stop, int32_t* n_events, int32_t* events,
+                     int32_t events_cap);
+
+/* ---- channel -----------------------------------------------------------
+ * decode_trial's frame generation (src/sim_harness.cpp:67-73): per trial
+ * TrialRng(seed, trial) (src/channel.cpp:31-41), K info bits, encode,
+ * BPSK, AWGN at Eb/N0 with rate k/n, LLR = 2y/sigma^2 in fp64, stored as
+ * fp32 (and fp64 when llr64_dev != NULL). u_dev (optional) receives the
+ * transmitted source word u bit-packed (frames x ceil(n/32)). Device
+ * pointers, asynchronous on `stream`. */
+int pbp_generate_device(pbp_ctx* ctx, const pbp_code* code, uint64_t seed, int64_t first_trial,
+                        int64_t count, double ebn0_db, int noiseless, float* llr_dev,
+                        double* llr64_dev, uint32_t* u_dev, void* stream);
+/* Host-buffer convenience wrapper of pbp_generate_device. */
+int pbp_generate(pbp_ctx* ctx, const pbp_code* code, uint64_t seed, int64_t first_trial,
+                 int64_t count, double ebn0_db, int noiseless, float* llr, double* llr64,
+                 uint32_t* u_bits);
+
+/* ---- Monte-Carlo point (run_point, src/sim_harness.cpp:129-186, with
+ *      min_frame_errors = infinity): trials [first_trial, first_trial+frames)
+ *      generated on the device, decoded, counters accumulated on the device.
+ *      Shard trial ranges across GPUs and sum the counters (one int64
+ *      allreduce) for the multi-GPU run. */
+int pbp_simulate_point(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed,
+                       int64_t first_trial, int64_t frames, double ebn0_db, int noiseless,
+                       float alpha, int32_t max_iter, pbp_counters* out);
+/* Device-side variant: counters (10 int64) accumulate into counters_dev
+ * (not cleared); asynchronous on `stream`. */
+int pbp_simulate_point_device(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed,
+                              int64_t first_trial, int64_t frames, double ebn0_db,
+                              int noiseless, float alpha, int32_t max_iter,
+                              int64_t* counters_dev, void* stream);
+
+/* Counter accumulation for already-generated frames (device pointers):
+ * decodes llrs_dev and compares against u_dev (from pbp_generate_device). */
+int pbp_decode_count_device(pbp_ctx* ctx, const pbp_code* code, int decoder,
+                            const float* llrs_dev, const uint32_t* u_dev, int64_t frames,
+                            float alpha, int32_t max_iter, int64_t* counters_dev, void* stream);
+
+/* Which kernel serves a code length: 1 = warp-resident fast path,
+ * 0 = CTA generic path. For tests and bench introspection. */
+int pbp_kernel_path(int32_t n);
+/* Route every decode of this context through the generic kernel (on != 0).
+ * Test hook: lets the suite check both kernels against the oracle. */
+int pbp_ctx_force_generic(pbp_ctx* ctx, int on);
+/* Launch statistics of the last decode on this context (kernel launches,
+ * frames re-routed to the generic kernel because |LLR| exceeded the
+ * clamp-free bound or was not finite). */
+int pbp_last_launch_info(pbp_ctx* ctx, int32_t* launches, int64_t* rerouted_frames);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

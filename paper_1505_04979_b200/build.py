@@ -1,0 +1,85 @@
+"""In-tree build of libpbp.so (CUDA kernels for sm_100a + C ABI + C++ host API).
+
+Run as ``python -m paper_1505_04979_b200.build`` or via ``__graft_entry__.build()``.
+Objects go to build/, the shared library to paper_1505_04979_b200/_lib/ so it
+travels to the GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OBJ = os.path.join(ROOT, "build", "obj")
+LIB_DIR = os.path.join(PKG, "_lib")
+LIB = os.path.join(LIB_DIR, "libpbp.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+                  "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
+                  "-I", os.path.join(ROOT, "include")]
+CXXFLAGS = ["-O3", "-std=c++20", "-fPIC", "-I", os.path.join(ROOT, "include"),
+            "-I", "/usr/local/cuda/include"]
+
+
+def _sources():
+    cu = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
+    cpp = sorted(f for f in os.listdir(CSRC) if f.endswith(".cpp"))
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".hpp"))]
+    deps += [os.path.join(ROOT, "include", "pbp.h")]
+    inc = os.path.join(ROOT, "include", "polarbp")
+    if os.path.isdir(inc):
+        deps += [os.path.join(inc, f) for f in os.listdir(inc)]
+    return cu, cpp, deps
+
+
+def _stale(obj, src, deps):
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    return any(os.path.getmtime(p) > t for p in [src] + deps)
+
+
+def build(verbose=False, jobs=None):
+    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(LIB_DIR, exist_ok=True)
+    cu, cpp, deps = _sources()
+    cmds, objs = [], []
+    for f in cu:
+        src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
+        objs.append(obj)
+        if _stale(obj, src, deps):
+            cmds.append([NVCC] + NVFLAGS + ["-c", src, "-o", obj])
+    for f in cpp:
+        src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
+        objs.append(obj)
+        if _stale(obj, src, deps):
+            cmds.append(["g++"] + CXXFLAGS + ["-c", src, "-o", obj])
+    procs = []
+    for c in cmds:
+        if verbose:
+            print(" ".join(c), flush=True)
+        procs.append((c, subprocess.Popen(c, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
+    failed = False
+    for c, p in procs:
+        out = p.communicate()[0].decode()
+        if p.returncode != 0:
+            failed = True
+            sys.stderr.write(out)
+        elif verbose and out.strip():
+            print(out)
+    if failed:
+        raise RuntimeError("libpbp build failed")
+    if cmds or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
+        link = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
+        if verbose:
+            print(" ".join(link), flush=True)
+        subprocess.run(link, check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose=True))

@@ -1,0 +1,632 @@
+// C ABI of libpbp.so (include/pbp.h): device context, argument checking
+// with the reference's exception texts, kernel orchestration and the
+// host-side code helpers (construction, transform, encode).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/pbp.h"
+#include "pbp_common.cuh"
+
+namespace pbp {
+// kernels (bp_generic.cu, bp_warp.cu, channel.cu)
+cudaError_t launch_generic(const DecodeArgs& a, int grid, cudaStream_t stream);
+size_t generic_smem_bytes(int n);
+long long generic_scratch_floats(int n, int m);
+cudaError_t launch_warp(const DecodeArgs& a, int grid, cudaStream_t st);
+int warp_kernel_supported(int m);
+int warp_blocks_per_sm(int m, int kind);
+cudaError_t launch_channel(const GenArgs& g, int grid, cudaStream_t stream);
+}  // namespace pbp
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int status, const std::string& msg) {
+    g_err = msg;
+    return status;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(PBP_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define PBP_CUDA(call)                                   \
+    do {                                                 \
+        cudaError_t e_ = (call);                         \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+bool is_pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
+
+int log2i(int n) {
+    int m = 0;
+    while ((1 << m) < n) ++m;
+    return m;
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t count) {
+        if (count <= cap) return PBP_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(count, 1);
+        cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+        cap = want;
+        return PBP_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace
+
+struct pbp_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;
+    // code tables
+    std::vector<uint8_t> code_key;
+    int n = 0, m = 0, k = 0;
+    DevBuf<uint32_t> frozen_bits;
+    DevBuf<uint8_t> frozen_rows;
+    DevBuf<int> info_rows;
+    // work queue + re-route list
+    DevBuf<unsigned long long> ctl;  // [0] warp queue, [1] generic queue, [2] list length
+    DevBuf<long long> list;
+    DevBuf<float> scratch;
+    DevBuf<unsigned long long> counters;
+    // host-API staging
+    DevBuf<float> llr;
+    DevBuf<uint32_t> ubits, truth;
+    DevBuf<int> iters, nev, events;
+    DevBuf<long long> pe;
+    DevBuf<uint8_t> stop;
+    int last_launches = 0;
+    int force_generic = 0;
+};
+
+namespace {
+
+int check_code(const pbp_code* code) {
+    if (!code || !code->frozen) return fail(PBP_EINVAL, "pbp_code: null code or frozen mask");
+    if (!is_pow2(code->n) || code->n > (1 << 24))
+        return fail(PBP_EINVAL, "pbp_code: n must be a power of two <= 2^24");
+    if (code->m != log2i(code->n)) return fail(PBP_EINVAL, "pbp_code: m != log2(n)");
+    int frozen = 0;
+    for (int i = 0; i < code->n; ++i) frozen += code->frozen[i] ? 1 : 0;
+    if (code->k != code->n - frozen)
+        return fail(PBP_EINVAL, "pbp_code: k inconsistent with the frozen mask");
+    if (code->k < 1) return fail(PBP_EINVAL, "from_frozen_mask: no information positions");
+    return PBP_OK;
+}
+
+int upload_code(pbp_ctx* ctx, const pbp_code* code) {
+    int rc = check_code(code);
+    if (rc) return rc;
+    std::vector<uint8_t> key(code->frozen, code->frozen + code->n);
+    if (ctx->n == code->n && key == ctx->code_key) return PBP_OK;
+    const int n = code->n, nw = (n + 31) / 32;
+    std::vector<uint32_t> bits(nw, 0u);
+    std::vector<uint8_t> rows(n);
+    std::vector<int> info;
+    for (int r = 0; r < n; ++r) {
+        rows[r] = code->frozen[r] ? 1 : 0;
+        if (rows[r]) bits[r >> 5] |= 1u << (r & 31);
+        else info.push_back(r);
+    }
+    if ((rc = ctx->frozen_bits.ensure(nw)) || (rc = ctx->frozen_rows.ensure(n)) ||
+        (rc = ctx->info_rows.ensure(info.size())))
+        return rc;
+    PBP_CUDA(cudaMemcpyAsync(ctx->frozen_bits.p, bits.data(), nw * 4, cudaMemcpyHostToDevice, ctx->stream));
+    PBP_CUDA(cudaMemcpyAsync(ctx->frozen_rows.p, rows.data(), n, cudaMemcpyHostToDevice, ctx->stream));
+    PBP_CUDA(cudaMemcpyAsync(ctx->info_rows.p, info.data(), info.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    PBP_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->code_key = std::move(key);
+    ctx->n = n;
+    ctx->m = code->m;
+    ctx->k = code->k;
+    return PBP_OK;
+}
+
+struct DecodeReq {
+    int kind = 0;
+    const float* llr = nullptr;
+    long long frames = 0;
+    float alpha = 0.9375f;
+    int max_iter = 40;
+    uint32_t* u_bits = nullptr;
+    int* iters = nullptr;
+    long long* pe = nullptr;
+    uint8_t* stop = nullptr;
+    int* nev = nullptr;
+    int* events = nullptr;
+    int ev_cap = 0;
+    const uint32_t* truth = nullptr;
+    unsigned long long* counters = nullptr;
+    bool force_generic = false;
+};
+
+// Launch the decode of `frames` frames already on the device.
+int run_decode(pbp_ctx* ctx, const DecodeReq& r, cudaStream_t st) {
+    if (r.kind < 0 || r.kind > 2) return fail(PBP_EINVAL, "unknown decoder kind");
+    if (r.frames < 0) return fail(PBP_EINVAL, "frames < 0");
+    ctx->last_launches = 0;
+    if (r.frames == 0) return PBP_OK;
+    int rc;
+    if ((rc = ctx->ctl.ensure(4))) return rc;
+    PBP_CUDA(cudaMemsetAsync(ctx->ctl.p, 0, 4 * sizeof(unsigned long long), st));
+    pbp::DecodeArgs a{};
+    a.n = ctx->n;
+    a.m = ctx->m;
+    a.kind = r.kind;
+    a.max_iter = r.max_iter;
+    a.alpha = r.alpha;
+    a.frozen_bits = ctx->frozen_bits.p;
+    a.frozen_rows = ctx->frozen_rows.p;
+    a.llr = r.llr;
+    a.frames = r.frames;
+    a.u_bits = r.u_bits;
+    a.iters = r.iters;
+    a.pe = r.pe;
+    a.stop = r.stop;
+    a.nev = r.nev;
+    a.events = r.events;
+    a.ev_cap = r.ev_cap;
+    a.truth_u = r.truth;
+    a.counters = r.counters;
+    a.list_len = ctx->ctl.p + 2;
+
+    const bool fast = !r.force_generic && !ctx->force_generic && pbp::warp_kernel_supported(ctx->m);
+    long long generic_frames_max = r.frames;
+    if (fast) {
+        if ((rc = ctx->list.ensure(r.frames))) return rc;
+        a.list = ctx->list.p;
+        a.queue = ctx->ctl.p + 0;
+        a.list_mode = 0;
+        const int per_sm = std::max(1, pbp::warp_blocks_per_sm(ctx->m, r.kind));
+        const long long grid = std::min<long long>((long long)per_sm * ctx->sm_count, r.frames);
+        cudaError_t e = pbp::launch_warp(a, (int)grid, st);
+        if (e != cudaSuccess) return cuda_fail(e, "bp_warp_kernel launch");
+        ctx->last_launches += 1;
+        // frames the fast kernel re-routed (|LLR| beyond the clamp-free bound)
+        a.list_mode = 1;
+        generic_frames_max = std::min<long long>(r.frames, ctx->sm_count);
+    } else {
+        a.list = nullptr;
+        a.list_mode = 0;
+    }
+    a.queue = ctx->ctl.p + 1;
+    // generic kernel: bounded grid, per-CTA scratch
+    const long long stride = pbp::generic_scratch_floats(ctx->n, ctx->m);
+    long long grid = std::min<long long>(generic_frames_max, (long long)ctx->sm_count * 4);
+    const long long max_scratch_floats = 1ll << 28;  // 1 GiB
+    grid = std::max<long long>(1, std::min<long long>(grid, max_scratch_floats / stride));
+    if ((rc = ctx->scratch.ensure((size_t)(grid * stride)))) return rc;
+    a.scratch = ctx->scratch.p;
+    a.scratch_stride = stride;
+    cudaError_t e = pbp::launch_generic(a, (int)grid, st);
+    if (e != cudaSuccess) return cuda_fail(e, "bp_generic_kernel launch");
+    ctx->last_launches += 1;
+    return PBP_OK;
+}
+
+int run_generate(pbp_ctx* ctx, uint64_t seed, long long first, long long count, double ebn0,
+                 int noiseless, float* llr, double* llr64, uint32_t* u, cudaStream_t st) {
+    if (count < 0) return fail(PBP_EINVAL, "count < 0");
+    double sigma2 = 0.0;
+    int rc = pbp_noise_variance(ebn0, (double)ctx->k / ctx->n, &sigma2);
+    if (rc) return rc;
+    if (count == 0) return PBP_OK;
+    pbp::GenArgs g{};
+    g.n = ctx->n;
+    g.k = ctx->k;
+    g.seed = seed;
+    g.first = first;
+    g.count = count;
+    g.sigma = std::sqrt(sigma2);
+    g.scale = 2.0 / sigma2;
+    g.noiseless = noiseless;
+    g.info_rows = ctx->info_rows.p;
+    g.llr = llr;
+    g.llr64 = llr64;
+    g.u_out = u;
+    const long long grid = std::min<long long>((count + 3) / 4, (long long)ctx->sm_count * 8);
+    cudaError_t e = pbp::launch_channel(g, (int)std::max<long long>(grid, 1), st);
+    if (e != cudaSuccess) return cuda_fail(e, "channel_gen_kernel launch");
+    return PBP_OK;
+}
+
+cudaStream_t pick(pbp_ctx* ctx, void* s) { return s ? (cudaStream_t)s : ctx->stream; }
+
+}  // namespace
+
+extern "C" {
+
+const char* pbp_last_error(void) { return g_err.c_str(); }
+int pbp_version(void) { return PBP_VERSION; }
+
+int pbp_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+    return c;
+}
+
+int pbp_ctx_create(int device, pbp_ctx** out) {
+    if (!out) return fail(PBP_EINVAL, "pbp_ctx_create: out is null");
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        return fail(PBP_ENODEV, "no CUDA device available (libpbp has no CPU fallback)");
+    if (device < 0 || device >= count) return fail(PBP_EINVAL, "pbp_ctx_create: bad device index");
+    PBP_CUDA(cudaSetDevice(device));
+    auto* ctx = new pbp_ctx;
+    ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return cuda_fail(e, "cudaStreamCreate");
+    }
+    *out = ctx;
+    return PBP_OK;
+}
+
+int pbp_ctx_destroy(pbp_ctx* ctx) {
+    if (!ctx) return PBP_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->frozen_bits.release();
+    ctx->frozen_rows.release();
+    ctx->info_rows.release();
+    ctx->ctl.release();
+    ctx->list.release();
+    ctx->scratch.release();
+    ctx->counters.release();
+    ctx->llr.release();
+    ctx->ubits.release();
+    ctx->truth.release();
+    ctx->iters.release();
+    ctx->nev.release();
+    ctx->events.release();
+    ctx->pe.release();
+    ctx->stop.release();
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return PBP_OK;
+}
+
+void* pbp_ctx_stream(pbp_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int pbp_ctx_synchronize(pbp_ctx* ctx) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    PBP_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PBP_OK;
+}
+
+int pbp_ctx_force_generic(pbp_ctx* ctx, int on) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    ctx->force_generic = on ? 1 : 0;
+    return PBP_OK;
+}
+
+int pbp_kernel_path(int32_t n) { return is_pow2(n) && pbp::warp_kernel_supported(log2i(n)) ? 1 : 0; }
+
+int pbp_last_launch_info(pbp_ctx* ctx, int32_t* launches, int64_t* rerouted) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    if (launches) *launches = ctx->last_launches;
+    if (rerouted) {
+        *rerouted = 0;
+        if (ctx->ctl.p) {
+            unsigned long long v = 0;
+            PBP_CUDA(cudaStreamSynchronize(ctx->stream));
+            PBP_CUDA(cudaMemcpy(&v, ctx->ctl.p + 2, sizeof(v), cudaMemcpyDeviceToHost));
+            *rerouted = (int64_t)v;
+        }
+    }
+    return PBP_OK;
+}
+
+// ---- host-side code helpers ------------------------------------------------
+
+int pbp_construct(int32_t n, int32_t k, double design_z, uint8_t* frozen_out) {
+    // PolarCode::construct (src/polar_code.cpp:53-66) and bhattacharyya_profile (:27-43)
+    if (!is_pow2(n)) return fail(PBP_EINVAL, "construct: n must be a power of two");
+    if (k < 1 || k > n) return fail(PBP_EINVAL, "construct: k must satisfy 1 <= k <= n");
+    if (!(design_z > 0.0 && design_z < 1.0))
+        return fail(PBP_EINVAL, "bhattacharyya_profile: design_z must be in (0,1)");
+    if (!frozen_out) return fail(PBP_EINVAL, "construct: null output");
+    std::vector<double> z(n, design_z);
+    for (int half = n / 2; half >= 1; half /= 2)
+        for (int i = 0; i < n; ++i) {
+            if (i & half) continue;
+            const double zi = z[i];
+            z[i] = 2.0 * zi - zi * zi;  // degraded child keeps the lower index
+            z[i + half] = zi * zi;
+        }
+    std::vector<int> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&z](int a, int b) { return z[a] > z[b]; });
+    std::memset(frozen_out, 0, n);
+    for (int i = 0; i < n - k; ++i) frozen_out[order[i]] = 1;
+    return PBP_OK;
+}
+
+int pbp_polar_transform(uint8_t* v, int32_t n) {
+    if (n <= 0 || !is_pow2(n)) return fail(PBP_EINVAL, "polar_transform: length must be a power of two");
+    for (int half = 1; half < n; half <<= 1)
+        for (int i = 0; i < n; ++i)
+            if (!(i & half)) v[i] ^= v[i + half];
+    return PBP_OK;
+}
+
+int pbp_encode(const pbp_code* code, const uint8_t* info, uint8_t* u_out, uint8_t* x_out) {
+    int rc = check_code(code);
+    if (rc) return rc;
+    int next = 0;
+    for (int i = 0; i < code->n; ++i) u_out[i] = code->frozen[i] ? 0 : (info[next++] ? 1 : 0);
+    std::memcpy(x_out, u_out, code->n);
+    return pbp_polar_transform(x_out, code->n);
+}
+
+int pbp_noise_variance(double ebn0_db, double rate, double* out) {
+    // noise_variance (src/channel.cpp:9-15)
+    if (!(rate > 0.0 && rate <= 1.0)) return fail(PBP_EINVAL, "noise_variance: rate must be in (0,1]");
+    if (!std::isfinite(ebn0_db)) return fail(PBP_EINVAL, "noise_variance: ebn0_db must be finite");
+    *out = 1.0 / (2.0 * rate * std::pow(10.0, ebn0_db / 10.0));
+    return PBP_OK;
+}
+
+// ---- decode ------------------------------------------------------------------
+
+int pbp_decode_batch_device(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs_dev,
+                            int64_t frames, float alpha, int32_t max_iter, pbp_frame_out* out_dev,
+                            void* stream) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    PBP_CUDA(cudaSetDevice(ctx->device));
+    int rc = upload_code(ctx, code);
+    if (rc) return rc;
+    DecodeReq r;
+    r.kind = decoder;
+    r.llr = llrs_dev;
+    r.frames = frames;
+    r.alpha = alpha;
+    r.max_iter = max_iter;
+    if (out_dev) {
+        r.u_bits = out_dev->u_hat_bits;
+        r.iters = out_dev->iterations;
+        r.pe = reinterpret_cast<long long*>(out_dev->pe);
+        r.stop = out_dev->stop;
+        r.nev = out_dev->n_events;
+    }
+    return run_decode(ctx, r, pick(ctx, stream));
+}
+
+int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs,
+                     int64_t frames, float alpha, int32_t max_iter, pbp_frame_out* out) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    if (frames < 0) return fail(PBP_EINVAL, "frames < 0");
+    PBP_CUDA(cudaSetDevice(ctx->device));
+    int rc = upload_code(ctx, code);
+    if (rc) return rc;
+    const int n = ctx->n, nw = (n + 31) / 32;
+    if ((rc = ctx->llr.ensure((size_t)frames * n)) || (rc = ctx->ubits.ensure((size_t)frames * nw)) ||
+        (rc = ctx->iters.ensure(frames)) || (rc = ctx->pe.ensure(frames)) ||
+        (rc = ctx->stop.ensure(frames)) || (rc = ctx->nev.ensure(frames)))
+        return rc;
+    cudaStream_t st = ctx->stream;
+    if (frames > 0)
+        PBP_CUDA(cudaMemcpyAsync(ctx->llr.p, llrs, (size_t)frames * n * 4, cudaMemcpyHostToDevice, st));
+    DecodeReq r;
+    r.kind = decoder;
+    r.llr = ctx->llr.p;
+    r.frames = frames;
+    r.alpha = alpha;
+    r.max_iter = max_iter;
+    r.u_bits = ctx->ubits.p;
+    r.iters = ctx->iters.p;
+    r.pe = ctx->pe.p;
+    r.stop = ctx->stop.p;
+    r.nev = ctx->nev.p;
+    if ((rc = run_decode(ctx, r, st))) return rc;
+    if (out && frames > 0) {
+        if (out->u_hat_bits)
+            PBP_CUDA(cudaMemcpyAsync(out->u_hat_bits, ctx->ubits.p, (size_t)frames * nw * 4, cudaMemcpyDeviceToHost, st));
+        if (out->iterations)
+            PBP_CUDA(cudaMemcpyAsync(out->iterations, ctx->iters.p, (size_t)frames * 4, cudaMemcpyDeviceToHost, st));
+        if (out->pe) PBP_CUDA(cudaMemcpyAsync(out->pe, ctx->pe.p, (size_t)frames * 8, cudaMemcpyDeviceToHost, st));
+        if (out->stop) PBP_CUDA(cudaMemcpyAsync(out->stop, ctx->stop.p, (size_t)frames, cudaMemcpyDeviceToHost, st));
+        if (out->n_events)
+            PBP_CUDA(cudaMemcpyAsync(out->n_events, ctx->nev.p, (size_t)frames * 4, cudaMemcpyDeviceToHost, st));
+    }
+    PBP_CUDA(cudaStreamSynchronize(st));
+    return PBP_OK;
+}
+
+int pbp_decode_trace(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs, float alpha,
+                     int32_t max_iter, uint8_t* u_hat, int32_t* iterations, int64_t* pe, int32_t* stop,
+                     int32_t* n_events, int32_t* events, int32_t events_cap) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    PBP_CUDA(cudaSetDevice(ctx->device));
+    int rc = upload_code(ctx, code);
+    if (rc) return rc;
+    const int n = ctx->n, nw = (n + 31) / 32;
+    const int cap = std::max(events_cap, 1);
+    if ((rc = ctx->llr.ensure(n)) || (rc = ctx->ubits.ensure(nw)) || (rc = ctx->iters.ensure(1)) ||
+        (rc = ctx->pe.ensure(1)) || (rc = ctx->stop.ensure(1)) || (rc = ctx->nev.ensure(1)) ||
+        (rc = ctx->events.ensure((size_t)cap * 5)))
+        return rc;
+    cudaStream_t st = ctx->stream;
+    PBP_CUDA(cudaMemcpyAsync(ctx->llr.p, llrs, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    DecodeReq r;
+    r.kind = decoder;
+    r.llr = ctx->llr.p;
+    r.frames = 1;
+    r.alpha = alpha;
+    r.max_iter = max_iter;
+    r.u_bits = ctx->ubits.p;
+    r.iters = ctx->iters.p;
+    r.pe = ctx->pe.p;
+    r.stop = ctx->stop.p;
+    r.nev = ctx->nev.p;
+    r.events = ctx->events.p;
+    r.ev_cap = cap;
+    if ((rc = run_decode(ctx, r, st))) return rc;
+    std::vector<uint32_t> bits(nw);
+    int it = 0, sp8 = 0, ne = 0;
+    long long act = 0;
+    uint8_t s8 = 0;
+    PBP_CUDA(cudaMemcpyAsync(bits.data(), ctx->ubits.p, nw * 4, cudaMemcpyDeviceToHost, st));
+    PBP_CUDA(cudaMemcpyAsync(&it, ctx->iters.p, 4, cudaMemcpyDeviceToHost, st));
+    PBP_CUDA(cudaMemcpyAsync(&act, ctx->pe.p, 8, cudaMemcpyDeviceToHost, st));
+    PBP_CUDA(cudaMemcpyAsync(&s8, ctx->stop.p, 1, cudaMemcpyDeviceToHost, st));
+    PBP_CUDA(cudaMemcpyAsync(&ne, ctx->nev.p, 4, cudaMemcpyDeviceToHost, st));
+    std::vector<int> ev((size_t)cap * 5);
+    PBP_CUDA(cudaMemcpyAsync(ev.data(), ctx->events.p, ev.size() * 4, cudaMemcpyDeviceToHost, st));
+    PBP_CUDA(cudaStreamSynchronize(st));
+    sp8 = s8;
+    if (u_hat)
+        for (int r2 = 0; r2 < n; ++r2) u_hat[r2] = (bits[r2 >> 5] >> (r2 & 31)) & 1u;
+    if (iterations) *iterations = it;
+    if (pe) *pe = act;
+    if (stop) *stop = sp8;
+    if (n_events) *n_events = ne;
+    if (events && events_cap > 0)
+        std::memcpy(events, ev.data(), (size_t)std::min(ne, events_cap) * 5 * 4);
+    return PBP_OK;
+}
+
+// ---- channel -----------------------------------------------------------------
+
+int pbp_generate_device(pbp_ctx* ctx, const pbp_code* code, uint64_t seed, int64_t first_trial,
+                        int64_t count, double ebn0_db, int noiseless, float* llr_dev, double* llr64_dev,
+                        uint32_t* u_dev, void* stream) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    PBP_CUDA(cudaSetDevice(ctx->device));
+    int rc = upload_code(ctx, code);
+    if (rc) return rc;
+    return run_generate(ctx, seed, first_trial, count, ebn0_db, noiseless, llr_dev, llr64_dev, u_dev,
+                        pick(ctx, stream));
+}
+
+int pbp_generate(pbp_ctx* ctx, const pbp_code* code, uint64_t seed, int64_t first_trial, int64_t count,
+                 double ebn0_db, int noiseless, float* llr, double* llr64, uint32_t* u_bits) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    if (count < 0) return fail(PBP_EINVAL, "count < 0");
+    PBP_CUDA(cudaSetDevice(ctx->device));
+    int rc = upload_code(ctx, code);
+    if (rc) return rc;
+    const int n = ctx->n, nw = (n + 31) / 32;
+    float* d_llr = nullptr;
+    double* d_llr64 = nullptr;
+    uint32_t* d_u = nullptr;
+    PBP_CUDA(cudaMalloc(&d_llr, std::max<size_t>(1, (size_t)count * n * 4)));
+    if (llr64) PBP_CUDA(cudaMalloc(&d_llr64, std::max<size_t>(1, (size_t)count * n * 8)));
+    if (u_bits) PBP_CUDA(cudaMalloc(&d_u, std::max<size_t>(1, (size_t)count * nw * 4)));
+    rc = run_generate(ctx, seed, first_trial, count, ebn0_db, noiseless, d_llr, d_llr64, d_u, ctx->stream);
+    if (!rc && count > 0) {
+        cudaStream_t st = ctx->stream;
+        if (llr) cudaMemcpyAsync(llr, d_llr, (size_t)count * n * 4, cudaMemcpyDeviceToHost, st);
+        if (llr64) cudaMemcpyAsync(llr64, d_llr64, (size_t)count * n * 8, cudaMemcpyDeviceToHost, st);
+        if (u_bits) cudaMemcpyAsync(u_bits, d_u, (size_t)count * nw * 4, cudaMemcpyDeviceToHost, st);
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "pbp_generate");
+    }
+    cudaFree(d_llr);
+    if (d_llr64) cudaFree(d_llr64);
+    if (d_u) cudaFree(d_u);
+    return rc;
+}
+
+// ---- Monte-Carlo counters ------------------------------------------------------
+
+int pbp_decode_count_device(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs_dev,
+                            const uint32_t* u_dev, int64_t frames, float alpha, int32_t max_iter,
+                            int64_t* counters_dev, void* stream) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    PBP_CUDA(cudaSetDevice(ctx->device));
+    int rc = upload_code(ctx, code);
+    if (rc) return rc;
+    DecodeReq r;
+    r.kind = decoder;
+    r.llr = llrs_dev;
+    r.frames = frames;
+    r.alpha = alpha;
+    r.max_iter = max_iter;
+    r.truth = u_dev;
+    r.counters = reinterpret_cast<unsigned long long*>(counters_dev);
+    return run_decode(ctx, r, pick(ctx, stream));
+}
+
+int pbp_simulate_point_device(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed,
+                              int64_t first_trial, int64_t frames, double ebn0_db, int noiseless,
+                              float alpha, int32_t max_iter, int64_t* counters_dev, void* stream) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    if (frames < 0) return fail(PBP_EINVAL, "frames < 0");
+    PBP_CUDA(cudaSetDevice(ctx->device));
+    int rc = upload_code(ctx, code);
+    if (rc) return rc;
+    const int n = ctx->n, nw = (n + 31) / 32;
+    // chunk so the staging stays bounded (~256 MiB of LLRs)
+    const long long chunk = std::max<long long>(1, std::min<long long>(frames, (1ll << 26) / n));
+    if ((rc = ctx->llr.ensure((size_t)chunk * n)) || (rc = ctx->truth.ensure((size_t)chunk * nw))) return rc;
+    cudaStream_t st = pick(ctx, stream);
+    for (long long done = 0; done < frames; done += chunk) {
+        const long long c = std::min(chunk, frames - done);
+        if ((rc = run_generate(ctx, seed, first_trial + done, c, ebn0_db, noiseless, ctx->llr.p, nullptr,
+                               ctx->truth.p, st)))
+            return rc;
+        DecodeReq r;
+        r.kind = decoder;
+        r.llr = ctx->llr.p;
+        r.frames = c;
+        r.alpha = alpha;
+        r.max_iter = max_iter;
+        r.truth = ctx->truth.p;
+        r.counters = reinterpret_cast<unsigned long long*>(counters_dev);
+        if ((rc = run_decode(ctx, r, st))) return rc;
+    }
+    return PBP_OK;
+}
+
+int pbp_simulate_point(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed, int64_t first_trial,
+                       int64_t frames, double ebn0_db, int noiseless, float alpha, int32_t max_iter,
+                       pbp_counters* out) {
+    if (!ctx || !out) return fail(PBP_EINVAL, "null argument");
+    PBP_CUDA(cudaSetDevice(ctx->device));
+    int rc;
+    if ((rc = ctx->counters.ensure(pbp::kNumCounters))) return rc;
+    PBP_CUDA(cudaMemsetAsync(ctx->counters.p, 0, pbp::kNumCounters * 8, ctx->stream));
+    rc = pbp_simulate_point_device(ctx, code, decoder, seed, first_trial, frames, ebn0_db, noiseless, alpha,
+                                   max_iter, reinterpret_cast<int64_t*>(ctx->counters.p), ctx->stream);
+    if (rc) return rc;
+    unsigned long long c[pbp::kNumCounters];
+    PBP_CUDA(cudaMemcpyAsync(c, ctx->counters.p, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+    PBP_CUDA(cudaStreamSynchronize(ctx->stream));
+    out->frames = (int64_t)c[pbp::kCntFrames];
+    out->bit_errors = (int64_t)c[pbp::kCntBitErr];
+    out->frame_errors = (int64_t)c[pbp::kCntFrameErr];
+    out->sum_iters = (int64_t)c[pbp::kCntIters];
+    out->sum_iters_sq = (int64_t)c[pbp::kCntItersSq];
+    out->sum_pe = (int64_t)c[pbp::kCntPe];
+    out->sum_events = (int64_t)c[pbp::kCntEvents];
+    for (int i = 0; i < 3; ++i) out->stop_hist[i] = (int64_t)c[pbp::kCntStop0 + i];
+    return PBP_OK;
+}
+
+}  // extern "C"

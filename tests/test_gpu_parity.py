@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA decoders through the C ABI against the oracle.
+
+Bar (north star): hard decisions, iteration counts, PE-activation counts, stop
+reasons and freeze-event counts bit-exact against the reference's fp32
+operation order ("ref32"), on the golden frames and on random inputs; both the
+warp-resident kernel and the generic kernel; property checks at full size.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1505_04979_b200 as P
+from conftest import load_manifest
+
+pytestmark = pytest.mark.gpu
+MAN = load_manifest()
+Z0 = math.exp(-0.5)
+
+
+def _cmp(r, golden, name, tag="ref32"):
+    n = golden[name + "/frozen"].size
+    got_u = P.unpack_bits(r["u_hat_bits"], n)
+    exp_u = np.unpackbits(golden[f"{name}/{tag}/u_hat"], axis=1, bitorder="little")[:, :n]
+    bad = np.flatnonzero((got_u != exp_u).any(1))
+    assert bad.size == 0, f"{name}: u_hat differs on frames {bad[:10]}"
+    for f in ("iterations", "pe", "stop", "n_events"):
+        g = r[f].astype(np.int64)
+        e = golden[f"{name}/{tag}/{f}"].astype(np.int64)
+        assert np.array_equal(g, e), f"{name}: {f} differs at {np.flatnonzero(g != e)[:10]}"
+
+
+@pytest.mark.parametrize("generic", [False, True], ids=["auto", "generic"])
+@pytest.mark.parametrize("case", MAN["cases"], ids=lambda c: c["name"])
+def test_golden_case(ctx, golden, case, generic):
+    name = case["name"]
+    code = P.PolarCode.from_frozen_mask(case["n"], golden[name + "/frozen"])
+    ctx.force_generic(generic)
+    try:
+        r = P.decode_batch(code, case["decoder"], golden[name + "/llr32"], 0.9375, case["max_iter"], ctx=ctx)
+    finally:
+        ctx.force_generic(False)
+    _cmp(r, golden, name)
+
+
+@pytest.mark.parametrize("generic", [False, True], ids=["auto", "generic"])
+def test_event_traces(ctx, golden, generic):
+    ctx.force_generic(generic)
+    try:
+        for ec in MAN["event_cases"]:
+            for i in range(ec["frames"]):
+                p = f"{ec['name']}/{i}"
+                fz = golden[p + "/frozen"]
+                code = P.PolarCode.from_frozen_mask(fz.size, fz)
+                events = []
+                out = P.decode_csfg(code, golden[p + "/llr32"], 0.9375, ec["max_iter"], events=events, ctx=ctx)
+                exp = golden[p + "/events"].reshape(-1, 5)
+                got = np.array([[e.iteration, e.stage, e.block, e.start, e.size] for e in events],
+                               np.int64).reshape(-1, 5)
+                assert np.array_equal(got, exp), p
+                assert [out.iterations_used, out.pe_activations, out.stop_reason, out.n_events] == \
+                    list(golden[p + "/meta"]), p
+                assert np.array_equal(out.u_hat, golden[p + "/u_hat"]), p
+    finally:
+        ctx.force_generic(False)
+
+
+def test_reference_known_answers(ctx):
+    # test_bp_core.cpp:185-204, test_csfg_freeze.cpp:222-246
+    code = P.PolarCode.construct(8, 4, 0.5)
+    o = P.decode_baseline(code, np.full(8, 2.0), 0.9375, 40, ctx=ctx)
+    assert (o.iterations_used, o.pe_activations, o.stop_reason) == (40, 480, 0)
+    assert not o.u_hat.any() and not o.info_bits.any()
+    o = P.decode_gmatrix(code, np.full(8, 2.0), 0.9375, 40, ctx=ctx)
+    assert (o.iterations_used, o.pe_activations, o.stop_reason) == (1, 12, 1)
+    ev = []
+    o = P.decode_csfg(code, np.full(8, 5.0), 0.9375, 40, events=ev, ctx=ctx)
+    assert (o.iterations_used, o.pe_activations, o.stop_reason) == (1, 7, 1)
+    assert [(e.stage, e.start, e.size) for e in ev] == [(0, 0, 4), (1, 4, 2), (2, 6, 1)]
+    with pytest.raises(ValueError):
+        P.decode_csfg(code, np.zeros(7), 0.9375, 40, ctx=ctx)  # init_state: LLR length != n
+
+
+@pytest.mark.parametrize("n", [2, 8, 32, 64, 128, 256, 512, 1024, 2048])
+@pytest.mark.parametrize("kind", ["baseline", "gmatrix", "csfg"])
+def test_random_llrs_vs_oracle(ctx, n, kind):
+    """Gaussian LLRs at several scales, exact zeros and exact ties, vs the C oracle (fp32)."""
+    rng = np.random.default_rng(1000 * n + len(kind))
+    fz = O.construct(n, max(1, n // 2), Z0)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    frames = 64 if n <= 1024 else 8
+    llr = rng.normal(1.0, 1.5, size=(frames, n)).astype(np.float32)
+    llr[: frames // 4] *= 8.0
+    llr[frames // 4: frames // 2, ::5] = 0.0
+    llr[frames // 2: 3 * frames // 4] = np.round(llr[frames // 2: 3 * frames // 4])  # ties
+    exp = O.decode_batch(kind, fz, llr, 0.9375, 25, prec=32)
+    got = P.decode_batch(code, kind, llr, 0.9375, 25, ctx=ctx)
+    assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"])
+    for f in ("iterations", "pe", "stop", "n_events"):
+        assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), f
+
+
+@pytest.mark.parametrize("n", [256, 1024])
+def test_clamp_and_nonfinite_frames_rerouted(ctx, n):
+    """Frames the clamp-free fast path cannot take go to the generic kernel (clamps kept)."""
+    rng = np.random.default_rng(7)
+    fz = O.construct(n, n // 2, Z0)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    llr = rng.normal(1.0, 1.0, size=(16, n)).astype(np.float32)
+    llr[1, 3] = 1e30
+    llr[2, :] *= 1e28
+    llr[3, 10] = -3e38
+    llr[4, 0] = 2e14
+    for kind in ("baseline", "gmatrix", "csfg"):
+        exp = O.decode_batch(kind, fz, llr, 0.9375, 20, prec=32)
+        got = P.decode_batch(code, kind, llr, 0.9375, 20, ctx=ctx)
+        launches, rerouted = ctx.last_launch_info()
+        assert rerouted == 4
+        assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"]), kind
+        for f in ("iterations", "pe", "stop", "n_events"):
+            assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), (kind, f)
+
+
+@pytest.mark.parametrize("n,seed,ebn0", [(64, 4242, 2.0), (1024, 2, 3.0), (256, 5, 2.5), (4096, 4, 2.5)])
+def test_channel_generation_matches_reference_stream(ctx, n, seed, ebn0):
+    fz = O.construct(n, n // 2, Z0 if n != 64 else 0.5)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    count = 48 if n <= 1024 else 8
+    llr, u, l64 = P.generate(code, seed, 3, count, ebn0, want64=True, ctx=ctx)
+    info, ref64 = O.trials(seed, 3, count, fz, ebn0, lib=O.C)
+    # transmitted words: bit-exact (integer RNG + GF(2) encode)
+    ref_u = np.zeros((count, n), np.uint8)
+    ref_u[:, fz == 0] = info
+    assert np.array_equal(P.unpack_bits(u, n), ref_u)
+    # fp32 LLRs the decoder consumes: exact; fp64 may differ in the last ulp (CUDA vs glibc log/cos)
+    assert np.array_equal(llr, ref64.astype(np.float32))
+    ulp = np.abs(l64 - ref64) / np.spacing(np.abs(ref64))
+    assert ulp.max() <= 4.0
+
+
+def test_simulate_point_counters_match_oracle(ctx):
+    n, seed, ebn0, frames = 1024, 2, 2.5, 384
+    fz = O.construct(n, n // 2, Z0)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    info, llr = O.trials(seed, 0, frames, fz, ebn0, lib=O.C)
+    for kind in ("baseline", "gmatrix", "csfg"):
+        c = P.simulate_point(code, kind, seed, 0, frames, ebn0, ctx=ctx)
+        r = O.decode_batch(kind, fz, llr.astype(np.float32), 0.9375, 40, prec=32)
+        be = (r["u_hat"][:, fz == 0] != info).sum(1)
+        it = r["iterations"].astype(np.int64)
+        assert c["frames"] == frames
+        assert c["bit_errors"] == int(be.sum())
+        assert c["frame_errors"] == int((be > 0).sum())
+        assert c["sum_iters"] == int(it.sum()) and c["sum_iters_sq"] == int((it * it).sum())
+        assert c["sum_pe"] == int(r["pe"].sum())
+        assert c["sum_events"] == int(r["n_events"].sum())
+        assert [c["stop_max_iter"], c["stop_gmatrix"], c["stop_csfg"]] == \
+            [int((r["stop"] == s).sum()) for s in range(3)]
+
+
+def test_sharded_counters_sum_to_whole(ctx):
+    """Trial-range sharding (the multi-GPU split) leaves the integer sums unchanged."""
+    code = P.PolarCode.construct(1024, 512, Z0)
+    whole = P.simulate_point(code, "csfg", 5, 0, 6000, 2.5, ctx=ctx)
+    parts = [P.simulate_point(code, "csfg", 5, a, b - a, 2.5, ctx=ctx) for a, b in ((0, 1500), (1500, 4100), (4100, 6000))]
+    for k in whole:
+        assert whole[k] == sum(p[k] for p in parts), k
+
+
+def test_full_size_properties(ctx):
+    """Config 2 at 3 dB, 1e5 frames: size-independent invariants."""
+    n, frames = 1024, 100_000
+    code = P.PolarCode.construct(n, 512, Z0)
+    llr, u, _ = P.generate(code, 2, 0, frames, 3.0, ctx=ctx)
+    r = P.decode_batch(code, "csfg", llr, 0.9375, 40, ctx=ctx)
+    bits = P.unpack_bits(r["u_hat_bits"], n)
+    assert not bits[:, code.frozen == 1].any()                      # frozen-bit safety
+    it, pe, stop = r["iterations"], r["pe"], r["stop"]
+    assert ((it >= 1) & (it <= 40)).all()
+    assert (pe <= it.astype(np.int64) * 10 * 512).all() and (pe > 0).all()
+    assert ((stop != 0) | (it == 40)).all()                            # max_iter stop => 40 iterations
+    truth = P.unpack_bits(u, n)
+    fer = (bits != truth).any(1).mean()
+    assert fer < 0.03                                                 # reference FER ~0.014 at 3 dB
+    r2 = P.decode_batch(code, "csfg", llr, 0.9375, 40, ctx=ctx)      # determinism
+    for f in r:
+        assert np.array_equal(r[f], r2[f]), f
+    # sample parity against the oracle on a strided subset of the full batch
+    idx = np.arange(0, frames, 997)
+    exp = O.decode_batch("csfg", code.frozen, llr[idx], 0.9375, 40, prec=32)
+    assert np.array_equal(bits[idx], exp["u_hat"])
+    assert np.array_equal(it[idx], exp["iterations"]) and np.array_equal(pe[idx], exp["pe"])
+
+
+def test_noiseless_all_decoders(ctx):
+    code = P.PolarCode.construct(1024, 512, Z0)
+    llr, u, _ = P.generate(code, 1, 0, 256, 1.0, noiseless=True, ctx=ctx)
+    for kind, it in (("baseline", 40), ("gmatrix", 1), ("csfg", 1)):
+        r = P.decode_batch(code, kind, llr, 0.9375, 40, ctx=ctx)
+        assert np.array_equal(r["u_hat_bits"], u), kind
+        assert (r["iterations"] == it).all(), kind
+
+
+def test_edge_cases(ctx):
+    code = P.PolarCode.construct(1024, 512, Z0)
+    llr = np.random.default_rng(3).normal(1, 1, size=(4, 1024)).astype(np.float32)
+    for kind in ("baseline", "gmatrix", "csfg"):
+        for mi in (0, 1, 2):
+            exp = O.decode_batch(kind, code.frozen, llr, 0.9375, mi, prec=32)
+            got = P.decode_batch(code, kind, llr, 0.9375, mi, ctx=ctx)
+            assert np.array_equal(P.unpack_bits(got["u_hat_bits"], 1024), exp["u_hat"]), (kind, mi)
+            for f in ("iterations", "pe", "stop", "n_events"):
+                assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), (kind, mi, f)
+    empty = P.decode_batch(code, "csfg", np.zeros((0, 1024), np.float32), 0.9375, 40, ctx=ctx)
+    assert empty["iterations"].size == 0
+    # n = 1 and n = 2 codes
+    for n in (1, 2):
+        c = P.PolarCode.construct(n, 1, 0.5)
+        l = np.array([[-1.0] * n, [1.0] * n], np.float32)
+        for kind in ("baseline", "gmatrix", "csfg"):
+            exp = O.decode_batch(kind, c.frozen, l, 0.9375, 5, prec=32)
+            got = P.decode_batch(c, kind, l, 0.9375, 5, ctx=ctx)
+            assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"]), (n, kind)
+            assert np.array_equal(got["iterations"], exp["iterations"]), (n, kind)
