@@ -13,12 +13,15 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
+OBJ = os.path.join(ROOT, "build", os.environ.get("PBP_OBJ_SUBDIR", "obj"))
 LIB_DIR = os.path.join(PKG, "_lib")
-LIB = os.path.join(LIB_DIR, "libpbp.so")
+LIB = os.path.join(LIB_DIR, os.environ.get("PBP_LIB_NAME", "libpbp.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+# -fmad=false: the reference rounds every product and sum separately
+# (src/bp_core.cpp:21-30); ptxas would otherwise fuse mul.rn.f32x2 + add.rn.f32x2
+# into FFMA2 (observed), changing decisions after ~20 iterations.
+NVFLAGS = ARCH + os.environ.get("PBP_NVCC_EXTRA", "").split() + ["-O3", "-fmad=false", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                   "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
                   "-I", os.path.join(ROOT, "include")]
 CXXFLAGS = ["-O3", "-std=c++20", "-fPIC", "-I", os.path.join(ROOT, "include"),

@@ -9,28 +9,33 @@
 // never leaves the register file inside a pass:
 //   pass q register layout: row(lane, j) = lane_lo | j << b_q | lane_hi << (b_q+K)
 //   (b_0 = 5: row = lane + 32 j ; last pass b = 0: row = P*lane + j).
-// Between passes R(e) goes through a row-indexed, XOR-swizzled shared array
-// X that then holds L(e) in place (the two never live at the same time).
-// L(s) of stages inside a pass stays in registers (n <= 512, and n = 1024's
-// first pass) or in lane-private float4 shared slots (n = 1024's last pass).
+// Between passes R(e) goes through a padded row-indexed shared array X
+// (index = row + 4*(row/32): conflict-free scalar stores from pass 0 and
+// conflict-free 128-bit loads in the last pass, no address arithmetic) that
+// then holds L(e) in place. L(s) inside a pass stays in registers (n <= 512,
+// and n = 1024's first pass) or in lane-private float4 shared slots
+// (n = 1024's last pass).
 //
-// Exactness: the PE is Eq. (1) of
-// src/bp_core.cpp:18-32 in fp32 with min.xorsign.abs + mul/add rounded
-// separately (no FMA contraction); r_top = fma(alpha, m, +0) never yields
-// -0, so R's sign bit equals the reference's (v < 0) decision; clamps are
-// elided because frames with |LLR| > kClampFreeBound are re-routed to the
-// generic kernel, which keeps them.
+// Arithmetic: Eq. (1) of src/bp_core.cpp:18-32 in fp32, two PEs at a time
+// with the packed FADD2 / FMUL2 / FFMA2 (add/mul/fma.rn.f32x2) and
+// min.xorsign.abs (FMNMX.XORSIGN): 6 issue slots per PE, every product and
+// sum rounded separately as in the reference (no contraction).
+// r_top = fma(alpha, m, +0) never yields -0, so R's sign bit equals the
+// reference's (v < 0) decision; clamps are elided
+// because frames with |LLR| > kClampFreeBound are re-routed to the generic
+// kernel, which keeps them.
 //
 // The csfg schedule (src/csfg_freeze.cpp:99-152) is followed literally:
 // after each stage the candidate block containing the frontier is checked
-// on the fresh R(s+1) (sign bits packed per lane, XOR butterfly along the
-// block's row bits: in-word for register bits, shfl_xor for lane bits),
-// committed, and the PE mask takes effect from the next stage on. Inactive
-// PEs are computed anyway (their outputs are never read by an active PE);
-// only the saturated boundary L(f+1) of a frozen block must survive, which
-// is enforced per storage class (read-side override for register arrays,
-// predicated stores for shared slots, re-saturation for X). PE activations
-// are counted by the reference rule from per-stage inactive-row counts.
+// on the fresh R(s+1) (sign bits of only the block's registers packed with
+// funnel shifts, XOR butterfly along the block's row bits: in-word for
+// register bits, shfl_xor for lane bits), committed, and the PE mask takes
+// effect from the next stage on. Inactive PEs are computed anyway (their
+// outputs are never read by an active PE); only the saturated boundary
+// L(f+1) of a frozen block must survive, enforced per storage class
+// (read-side override for register arrays, predicated stores for shared
+// slots, re-saturation for X). PE activations are counted by the reference
+// rule from per-stage inactive-row counts.
 #include "pbp_common.cuh"
 
 namespace pbp {
@@ -46,6 +51,7 @@ struct Plan {
     static constexpr int K = M - 5;
     static constexpr int Q = (M + K - 1) / K;
     static constexpr int NW = N / 32;
+    static constexpr int NX = N + N / 8;  // padded boundary array
     static constexpr int base_bit(int q) { return (M - K - q * K) > 0 ? (M - K - q * K) : 0; }
     static constexpr int pass_of(int s) { return s / K; }
     static constexpr int first(int q) { return q * K; }
@@ -82,21 +88,26 @@ struct Plan {
     }
     static constexpr int NLR = n_reg() > 0 ? n_reg() : 1;
     static constexpr int NLS = n_smem() > 0 ? n_smem() : 1;
+    // protection-mask slot of array L(s): register arrays first, then shared ones
+    static constexpr int prot_slot(int s) { return local_reg(s) ? reg_slot(s) : NLR + smem_slot(s); }
 };
 
 template <int M>
 struct WarpSmem {
     using PL = Plan<M>;
-    float R0[PL::N];                       // channel LLRs, row order
-    float X[PL::Q - 1][PL::N];             // pass boundaries: R(e) then L(e), swizzled rows
+    float4 R0p[PL::P / 4][32];             // channel LLRs, lane-private pass-0 layout
+    float X[PL::Q - 1][PL::NX];            // pass boundaries: R(e) then L(e), padded rows
     float4 Ls[PL::NLS][PL::P / 4][32];     // lane-private L slots (last pass, n=1024)
     float4 LM[PL::P / 4][32];              // L(m), lane-private, last-pass layout
+    uint32_t pm[PL::NLR + PL::NLS][32];    // per lane: rows whose L(s) is a frozen boundary
+    uint32_t ss[PL::NLR][32];              // ... and their signs (register arrays)
     uint32_t dec_u[PL::NW];                // decided_u bits (row order)
     uint32_t sat[PL::NW];                  // x_hat of the latest commit per row
     uint32_t xprot[PL::Q - 1][PL::NW];     // per boundary: blocks frozen at stage e-1
     int inact[32];                         // inactive top rows per stage
     int tmp[32];
     unsigned long long cnt[16];            // per-warp counter accumulators
+    uint32_t prot_any;                     // bit per prot slot: some lane has a protected row
     uint8_t fst[PL::N];                    // freeze_stage per row
 };
 
@@ -106,22 +117,37 @@ __device__ __forceinline__ float xsmin(float a, float b) {
     return d;
 }
 
-__device__ __forceinline__ int xidx(int row) { return row ^ ((row >> 5) & 31); }
-
-__device__ __forceinline__ uint32_t signbit_u(float v) { return __float_as_uint(v) >> 31; }
+// packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2), round-to-nearest per lane half
+__device__ __forceinline__ void add2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+    asm("{ .reg .b64 a, b, d; mov.b64 a, {%2, %3}; mov.b64 b, {%4, %5}; add.rn.f32x2 d, a, b; mov.b64 {%0, %1}, d; }"
+        : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void mul2s(float& d0, float& d1, float s, float a0, float a1) {
+    asm("{ .reg .b64 a, b, d; mov.b64 a, {%2, %2}; mov.b64 b, {%3, %4}; mul.rn.f32x2 d, a, b; mov.b64 {%0, %1}, d; }"
+        : "=f"(d0), "=f"(d1) : "f"(s), "f"(a0), "f"(a1));
+}
+__device__ __forceinline__ void fma2s0(float& d0, float& d1, float s, float a0, float a1) {
+    // s * a + (+0): never -0
+    asm("{ .reg .b64 a, b, c, d; mov.b64 a, {%2, %2}; mov.b64 b, {%3, %4}; mov.b64 c, 0; "
+        "fma.rn.f32x2 d, a, b, c; mov.b64 {%0, %1}, d; }"
+        : "=f"(d0), "=f"(d1) : "f"(s), "f"(a0), "f"(a1));
+}
 
 __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-    const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
         const int s = 16 >> i;
+        const uint32_t m = i == 0 ? 0x0000FFFFu : i == 1 ? 0x00FF00FFu : i == 2 ? 0x0F0F0F0Fu
+                         : i == 3 ? 0x33333333u : 0x55555555u;
         const uint32_t y = __shfl_xor_sync(kFull, x, s);
-        if ((lane & s) == 0)
-            x = (x & masks[i]) | ((y & masks[i]) << s);
-        else
-            x = (x & ~masks[i]) | ((y >> s) & masks[i]);
+        x = (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y & m) << s));
     }
     return x;
+}
+
+__device__ __forceinline__ uint32_t jmask(int tp) {
+    return tp == 0 ? 0x55555555u : tp == 1 ? 0x33333333u : tp == 2 ? 0x0F0F0F0Fu
+         : tp == 3 ? 0x00FF00FFu : 0x0000FFFFu;
 }
 
 template <int M, int KIND>
@@ -130,32 +156,59 @@ struct Dec {
     static constexpr int N = PL::N, P = PL::P, K = PL::K, Q = PL::Q, NW = PL::NW;
 
     WarpSmem<M>* sm;
+    const DecodeArgs* a;
     int lane;
     float alpha;
-    const DecodeArgs* a;
 
     float R[P];
     float Lr[PL::NLR][P];
-    uint32_t PM[PL::NLR];   // register arrays: rows whose L must read as +-CAP
-    uint32_t SS[PL::NLR];   // ... and their signs
-    uint32_t PMW[PL::NLS];  // shared slots: rows whose L must not be overwritten
-    uint32_t FZ[Q];         // frozen rows per pass layout
-    uint32_t FZW;           // frozen word (row order) of this lane (lane < NW)
+    uint32_t FZ[Q];  // frozen rows per pass layout (bit j = row_of<q>(j))
 
-    int frontier, nev, it;
-    long long act;
-    uint32_t xq;            // channel-side decisions, pass-0 layout
+    int frontier, nev, it, inact_total;
+    long long act, frame_;
+    uint32_t xq;     // channel-side decisions of stage 0, permuted pass-0 layout
+    int xperm;       // lane holding row-order word `lane` of x_hat after transpose
 
     template <int q>
     __device__ __forceinline__ int row_of(int j) const {
         constexpr int b = PL::base_bit(q);
         return (lane & ((1 << b) - 1)) | (j << b) | ((lane >> b) << (b + K));
     }
+    __device__ __forceinline__ static int xpad(int row) { return row + 4 * (row >> 5); }
 
-    // ---- L(S) sources / sinks ----------------------------------------
+    // ---- boundary array access (R out of pass q / L into pass q) ----------
+    template <int q>
+    __device__ __forceinline__ void x_load(const float* X, float (&v)[P]) const {
+        if constexpr (PL::base_bit(q) == 0) {
+            const float4* p = reinterpret_cast<const float4*>(X + xpad(P * lane));
+#pragma unroll
+            for (int c = 0; c < P / 4; ++c) {
+                const float4 t = p[c];
+                v[4 * c] = t.x;
+                v[4 * c + 1] = t.y;
+                v[4 * c + 2] = t.z;
+                v[4 * c + 3] = t.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < P; ++j) v[j] = X[xpad(row_of<q>(j))];
+        }
+    }
+    template <int q>
+    __device__ __forceinline__ void x_store(float* X, const float (&v)[P]) const {
+        if constexpr (PL::base_bit(q) == 0) {
+            float4* p = reinterpret_cast<float4*>(X + xpad(P * lane));
+#pragma unroll
+            for (int c = 0; c < P / 4; ++c) p[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < P; ++j) X[xpad(row_of<q>(j))] = v[j];
+        }
+    }
+
+    // ---- L(T) as read by stage T-1 -----------------------------------------
     template <int T>
     __device__ __forceinline__ void load_L(float (&Lt)[P]) {
-        // L(T) as read by stage T-1 (layout of pass_of(T-1))
         constexpr int q = PL::pass_of(T - 1);
         if constexpr (T == M) {
 #pragma unroll
@@ -167,17 +220,16 @@ struct Dec {
                 Lt[4 * c + 3] = v.w;
             }
         } else if constexpr (PL::is_boundary(T)) {
-            constexpr int xs = PL::pass_of(T) - 1;
-#pragma unroll
-            for (int j = 0; j < P; ++j) Lt[j] = sm->X[xs][xidx(row_of<q>(j))];
+            x_load<q>(sm->X[PL::pass_of(T) - 1], Lt);
         } else if constexpr (PL::local_reg(T)) {
             constexpr int sl = PL::reg_slot(T);
 #pragma unroll
             for (int j = 0; j < P; ++j) Lt[j] = Lr[sl][j];
-            if (__any_sync(kFull, PM[sl] != 0u)) {
+            if (sm->prot_any & (1u << sl)) {  // uniform, rare: boundary rows read as +-CAP
+                const uint32_t pm = sm->pm[sl][lane], ss = sm->ss[sl][lane];
 #pragma unroll
                 for (int j = 0; j < P; ++j)
-                    if ((PM[sl] >> j) & 1u) Lt[j] = ((SS[sl] >> j) & 1u) ? -kCap : kCap;
+                    if ((pm >> j) & 1u) Lt[j] = ((ss >> j) & 1u) ? -kCap : kCap;
             }
         } else {
             constexpr int sl = PL::smem_slot(T);
@@ -194,182 +246,240 @@ struct Dec {
 
     template <int S>
     __device__ __forceinline__ void store_L(const float (&Lt)[P]) {
-        constexpr int q = PL::pass_of(S);
         if constexpr (S == 0) {
             // L(0) is only consumed through x_hat (packed in the PE loop)
         } else if constexpr (PL::is_boundary(S)) {
-            constexpr int xs = PL::pass_of(S) - 1;
-#pragma unroll
-            for (int j = 0; j < P; ++j) sm->X[xs][xidx(row_of<q>(j))] = Lt[j];
+            x_store<PL::pass_of(S)>(sm->X[PL::pass_of(S) - 1], Lt);
         } else if constexpr (PL::local_reg(S)) {
             constexpr int sl = PL::reg_slot(S);
 #pragma unroll
             for (int j = 0; j < P; ++j) Lr[sl][j] = Lt[j];
         } else {
             constexpr int sl = PL::smem_slot(S);
+            constexpr int ps = PL::prot_slot(S);
             constexpr int d = 1 << (M - 1 - S);  // last pass: b = 0
-            const uint32_t pm = PMW[sl];
-            if (d >= 2) {
+            if (!(sm->prot_any & (1u << ps))) {
 #pragma unroll
                 for (int c = 0; c < P / 4; ++c)
-                    if (!((pm >> (4 * c)) & 1u))
-                        sm->Ls[sl][c][lane] = make_float4(Lt[4 * c], Lt[4 * c + 1], Lt[4 * c + 2], Lt[4 * c + 3]);
+                    sm->Ls[sl][c][lane] = make_float4(Lt[4 * c], Lt[4 * c + 1], Lt[4 * c + 2], Lt[4 * c + 3]);
             } else {
+                // frozen-boundary rows (blocks of >= 2 rows) keep their saturation
+                const uint32_t pm = sm->pm[ps][lane];
+                if (d >= 2) {
 #pragma unroll
-                for (int c = 0; c < P / 2; ++c)
-                    if (!((pm >> (2 * c)) & 1u))
-                        reinterpret_cast<float2*>(&sm->Ls[sl][c >> 1][lane])[c & 1] =
-                            make_float2(Lt[2 * c], Lt[2 * c + 1]);
-            }
-        }
-    }
-
-    // ---- re-saturation of boundary arrays (protected blocks) ----------
-    template <int QB>
-    __device__ __forceinline__ void resaturate() {
-        // boundary e = first(QB): blocks frozen at stage e-1 keep L(e) = +-CAP
-        constexpr int e = PL::first(QB);
-        constexpr int g = M - e;  // log2 block size
-        constexpr int nblk_words = ((1 << e) + 31) / 32;
-        bool touched = false;
-        for (int w = 0; w < nblk_words; ++w) {
-            uint32_t bits = sm->xprot[QB - 1][w];
-            while (bits) {
-                const int bi = 32 * w + __ffs(bits) - 1;
-                bits &= bits - 1;
-                touched = true;
-                for (int i = lane; i < (1 << g); i += 32) {
-                    const int row = (bi << g) + i;
-                    const bool neg = (sm->sat[row >> 5] >> (row & 31)) & 1u;
-                    sm->X[QB - 1][xidx(row)] = neg ? -kCap : kCap;
+                    for (int c = 0; c < P / 4; ++c)
+                        if (!((pm >> (4 * c)) & 1u))
+                            sm->Ls[sl][c][lane] = make_float4(Lt[4 * c], Lt[4 * c + 1], Lt[4 * c + 2], Lt[4 * c + 3]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < P / 2; ++c)
+                        if (!((pm >> (2 * c)) & 1u))
+                            reinterpret_cast<float2*>(&sm->Ls[sl][c >> 1][lane])[c & 1] =
+                                make_float2(Lt[2 * c], Lt[2 * c + 1]);
                 }
             }
         }
-        (void)touched;
+    }
+
+    // ---- re-saturation of a boundary array (blocks frozen at stage e-1) ---
+    template <int QB>
+    __device__ __forceinline__ void resaturate() {
+        constexpr int e = PL::first(QB);
+        constexpr int g = M - e;  // log2 block size
+        constexpr int nblk_words = ((1 << e) + 31) / 32;
+#pragma unroll 1
+        for (int w = 0; w < nblk_words; ++w) {
+            uint32_t bits = sm->xprot[QB - 1][w];
+#pragma unroll 1
+            while (bits) {
+                const int bi = 32 * w + __ffs(bits) - 1;
+                bits &= bits - 1;
+#pragma unroll 1
+                for (int i = lane; i < (1 << g); i += 32) {
+                    const int row = (bi << g) + i;
+                    const bool neg = (sm->sat[row >> 5] >> (row & 31)) & 1u;
+                    sm->X[QB - 1][xpad(row)] = neg ? -kCap : kCap;
+                }
+            }
+        }
         __syncwarp();  // X holds other lanes' L(e) writes of the previous iteration
     }
 
-    // ---- one PE stage ---------------------------------------------------
+    // ---- the PEs of stage S: two at a time with packed math --------------
     template <int S>
     __device__ __forceinline__ void pe_stage(float (&Lt)[P]) {
         constexpr int q = PL::pass_of(S);
         constexpr int t = (M - 1 - S) - PL::base_bit(q);
         constexpr int d = 1 << t;
+#ifdef PBP_SCALAR_PE
+        constexpr bool packed = false;
+#else
+        constexpr bool packed = true;
+#endif
+        if constexpr (d >= 2 && packed) {
 #pragma unroll
-        for (int j = 0; j < P; ++j) {
-            if (j & d) continue;
-            const float lt = Lt[j], lb = Lt[j + d], rt = R[j], rb = R[j + d];
-            const float cross = __fmul_rn(alpha, xsmin(lt, rt));
-            const float sum_bot = __fadd_rn(lb, rb);
-            const float l_top = __fmul_rn(alpha, xsmin(lt, sum_bot));
-            const float r_top = __fmaf_rn(alpha, xsmin(rt, sum_bot), 0.0f);
-            const float l_bot = __fadd_rn(lb, cross);
-            const float r_bot = __fadd_rn(rb, cross);
-            if constexpr (S == 0 && KIND != 0) {
-                xq |= signbit_u(__fadd_rn(rt, l_top)) << j;
-                xq |= signbit_u(__fadd_rn(rb, l_bot)) << (j + d);
+            for (int j = 0; j < P; j += 2) {
+                if (j & d) continue;
+                const float lt0 = Lt[j], lt1 = Lt[j + 1], lb0 = Lt[j + d], lb1 = Lt[j + d + 1];
+                const float rt0 = R[j], rt1 = R[j + 1], rb0 = R[j + d], rb1 = R[j + d + 1];
+                float c0, c1, s0, s1, lt0o, lt1o, rt0o, rt1o, lb0o, lb1o, rb0o, rb1o;
+                // products as fma(alpha, m, +0): ptxas fuses a bare mul.rn.f32x2 into a
+                // following add.rn.f32x2 (FFMA2, one rounding) even under -fmad=false;
+                // an FFMA2 with the zero register is the single-rounded product (it only
+                // turns a -0 product into +0, which changes no decision).
+                fma2s0(c0, c1, alpha, xsmin(lt0, rt0), xsmin(lt1, rt1));
+                add2(s0, s1, lb0, lb1, rb0, rb1);
+                fma2s0(lt0o, lt1o, alpha, xsmin(lt0, s0), xsmin(lt1, s1));
+                fma2s0(rt0o, rt1o, alpha, xsmin(rt0, s0), xsmin(rt1, s1));
+                add2(lb0o, lb1o, lb0, lb1, c0, c1);
+                add2(rb0o, rb1o, rb0, rb1, c0, c1);
+                if constexpr (S == 0 && KIND != 0) {
+                    // channel-side decisions (R(0) + L(0) < 0), pushed in a fixed order
+                    float x0, x1, x2, x3;
+                    add2(x0, x1, rt0, rt1, lt0o, lt1o);
+                    add2(x2, x3, rb0, rb1, lb0o, lb1o);
+                    xq = __funnelshift_l(__float_as_uint(x0), xq, 1);
+                    xq = __funnelshift_l(__float_as_uint(x1), xq, 1);
+                    xq = __funnelshift_l(__float_as_uint(x2), xq, 1);
+                    xq = __funnelshift_l(__float_as_uint(x3), xq, 1);
+                }
+                Lt[j] = lt0o;
+                Lt[j + 1] = lt1o;
+                Lt[j + d] = lb0o;
+                Lt[j + d + 1] = lb1o;
+                R[j] = rt0o;
+                R[j + 1] = rt1o;
+                R[j + d] = rb0o;
+                R[j + d + 1] = rb1o;
             }
-            Lt[j] = l_top;
-            Lt[j + d] = l_bot;
-            R[j] = r_top;
-            R[j + d] = r_bot;
+        } else {
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                if (j & d) continue;
+                const float lt = Lt[j], lb = Lt[j + d], rt = R[j], rb = R[j + d];
+                const float cross = __fmul_rn(alpha, xsmin(lt, rt));
+                const float sum_bot = __fadd_rn(lb, rb);
+                const float l_top = __fmul_rn(alpha, xsmin(lt, sum_bot));
+                const float l_bot = __fadd_rn(lb, cross);
+                if constexpr (S == 0 && KIND != 0) {
+                    xq |= (__float_as_uint(__fadd_rn(rt, l_top)) >> 31) << (P - 1 - xpush(j));
+                    xq |= (__float_as_uint(__fadd_rn(rb, l_bot)) >> 31) << (P - 1 - xpush(j + d));
+                }
+                Lt[j] = l_top;
+                R[j] = __fmaf_rn(alpha, xsmin(rt, sum_bot), 0.0f);
+                Lt[j + d] = l_bot;
+                R[j + d] = __fadd_rn(rb, cross);
+            }
         }
     }
 
-    // ---- csfg: candidate check + commit after stage S -------------------
+    // push index of stage-0 row-bit j in the packed x_hat order (see run())
+    __device__ __forceinline__ static constexpr int xpush(int j) {
+        return (j >= P / 2) ? 4 * ((j - P / 2) >> 1) + 2 + ((j - P / 2) & 1) : 4 * (j >> 1) + (j & 1);
+    }
+
+    // sign bits of R[J0 .. J0+W) packed at bits 0..W-1
+    template <int J0, int W>
+    __device__ __forceinline__ uint32_t pack_range() const {
+        uint32_t v = 0u;
+#pragma unroll
+        for (int i = W - 1; i >= 0; --i) v = __funnelshift_l(__float_as_uint(R[J0 + i]), v, 1);
+        return v;
+    }
+
+    template <int W, int G>
+    __device__ __forceinline__ uint32_t pack_block(int jb) const {
+        uint32_t v = 0u;
+#define PBP_CASE(i) \
+    case i:         \
+        if constexpr ((i) < G) v = pack_range<(i) * W, W>(); \
+        break;
+        switch (jb) {
+            PBP_CASE(0) PBP_CASE(1) PBP_CASE(2) PBP_CASE(3) PBP_CASE(4) PBP_CASE(5) PBP_CASE(6) PBP_CASE(7)
+            PBP_CASE(8) PBP_CASE(9) PBP_CASE(10) PBP_CASE(11) PBP_CASE(12) PBP_CASE(13) PBP_CASE(14) PBP_CASE(15)
+            PBP_CASE(16) PBP_CASE(17) PBP_CASE(18) PBP_CASE(19) PBP_CASE(20) PBP_CASE(21) PBP_CASE(22) PBP_CASE(23)
+            PBP_CASE(24) PBP_CASE(25) PBP_CASE(26) PBP_CASE(27) PBP_CASE(28) PBP_CASE(29) PBP_CASE(30) PBP_CASE(31)
+            default: break;
+        }
+#undef PBP_CASE
+        return v;
+    }
+
+    // ---- csfg: candidate check + commit after stage S ------------------------
     template <int S>
     __device__ __forceinline__ void check_commit() {
         constexpr int q = PL::pass_of(S);
         constexpr int b = PL::base_bit(q);
         constexpr int g = M - 1 - S;       // log2 block size
         constexpr int W = 1 << (g - b);    // registers per lane in a block
-        constexpr int hs = b + K - g;      // block-index bits above the register field
-        const int sz = 1 << g;
+        constexpr int hs = b + K - g;      // block-group bits within the lane
+        constexpr int G = 1 << hs;
         const int bi = frontier >> g;
-        const int start = bi << g;
-        // block membership of this lane's registers
-        const int lane_hi = lane >> b;
-        uint32_t msk = 0u;
-        if (lane_hi == (bi >> hs)) {
-            const uint32_t wmask = (W >= 32) ? 0xffffffffu : ((1u << W) - 1u);
-            msk = wmask << ((bi & ((1 << hs) - 1)) * W);
-        }
-        if constexpr (b < 5) {
-            // lanes whose low bits do not match the block are outside it
-            // only when g < b (never: g >= b); nothing to do
-        }
-        // x_hat bits of R(S+1)
-        uint32_t xb = 0u;
-#pragma unroll
-        for (int j = P - 1; j >= 0; --j) xb = __funnelshift_l(__float_as_uint(R[j]), xb, 1);
+        const int jb = bi & (G - 1);
+        const bool in_block = (lane >> b) == (bi >> hs);
+        const uint32_t xb = pack_block<W, G>(jb);
         uint32_t u = xb;
-        // butterfly along row bits 0 .. g-1
 #pragma unroll
         for (int gp = 0; gp < g; ++gp) {
             if (gp >= b) {
                 const int tp = gp - b;
-                const uint32_t jm = tp == 0 ? 0x55555555u : tp == 1 ? 0x33333333u
-                                  : tp == 2 ? 0x0F0F0F0Fu : tp == 3 ? 0x00FF00FFu : 0x0000FFFFu;
-                u ^= (u >> (1 << tp)) & jm;
+                u ^= (u >> (1 << tp)) & jmask(tp);
             } else {
                 const uint32_t o = __shfl_xor_sync(kFull, u, 1 << gp);
                 if (!((lane >> gp) & 1)) u ^= o;
             }
         }
-        const uint32_t viol = u & msk & FZ[q];
-        if (__any_sync(kFull, viol != 0u)) return;
-        commit<S>(bi, start, sz, msk, xb & msk, u & msk);
+        constexpr uint32_t wmask = W >= 32 ? 0xffffffffu : ((1u << W) - 1u);
+        const uint32_t fzb = (FZ[q] >> (jb * W)) & wmask;
+        if (__any_sync(kFull, in_block && (u & fzb))) return;
+        commit<S, W>(bi, jb, in_block, xb & wmask, u & wmask);
     }
 
-    template <int S>
-    __device__ __forceinline__ void commit(int bi, int start, int sz, uint32_t msk, uint32_t xbits,
-                                       uint32_t ubits) {
+    template <int S, int W>
+    __device__ __forceinline__ void commit(int bi, int jb, bool in_block, uint32_t xbits, uint32_t ubits) {
         constexpr int q = PL::pass_of(S);
         constexpr int b = PL::base_bit(q);
+        constexpr int g = M - 1 - S;
         constexpr int T = S + 1;
+        const int sz = 1 << g;
+        const int start = bi << g;
+        const int j0 = jb * W;
         // 1. saturate / protect L(S+1) (csfg_freeze.cpp:84-86)
-        if constexpr (T == M) {
-            uint32_t bits = msk;
-            while (bits) {
-                const int j = __ffs(bits) - 1;
-                bits &= bits - 1;
-                reinterpret_cast<float*>(&sm->LM[j >> 2][lane])[j & 3] = ((xbits >> j) & 1u) ? -kCap : kCap;
+        if constexpr (T == M || PL::local_smem(T)) {
+            float4* base;
+            if constexpr (T == M)
+                base = &sm->LM[0][0];
+            else
+                base = &sm->Ls[PL::smem_slot(T)][0][0];
+            if (in_block) {
+#pragma unroll 1
+                for (int i = 0; i < W; ++i) {
+                    const int j = j0 + i;
+                    reinterpret_cast<float*>(&base[(j >> 2) * 32 + lane])[j & 3] = ((xbits >> i) & 1u) ? -kCap : kCap;
+                }
+            }
+            if constexpr (T != M) {
+                constexpr int ps = PL::prot_slot(T);
+                const uint32_t msk = in_block ? (((W >= 32) ? 0xffffffffu : ((1u << W) - 1u)) << j0) : 0u;
+                sm->pm[ps][lane] |= msk;
+                if (__any_sync(kFull, msk != 0u) && lane == 0) sm->prot_any |= 1u << ps;
             }
         } else if constexpr (PL::is_boundary(T)) {
             constexpr int qb = PL::pass_of(T);
             if (lane == 0) sm->xprot[qb - 1][bi >> 5] |= 1u << (bi & 31);
-            scatter<q>(sm->sat, xbits, msk, start, sz);
-        } else if constexpr (PL::local_reg(T)) {
-            constexpr int sl = PL::reg_slot(T);
-            PM[sl] |= msk;
-            SS[sl] = (SS[sl] & ~msk) | xbits;
+            scatter<q, W>(sm->sat, xbits, in_block, j0, start, sz);
         } else {
-            constexpr int sl = PL::smem_slot(T);
-            PMW[sl] |= msk;
-            uint32_t bits = msk;
-            while (bits) {
-                const int j = __ffs(bits) - 1;
-                bits &= bits - 1;
-                reinterpret_cast<float*>(&sm->Ls[sl][j >> 2][lane])[j & 3] = ((xbits >> j) & 1u) ? -kCap : kCap;
-            }
+            constexpr int sl = PL::reg_slot(T);
+            const uint32_t msk = in_block ? (((W >= 32) ? 0xffffffffu : ((1u << W) - 1u)) << j0) : 0u;
+            sm->pm[sl][lane] |= msk;
+            sm->ss[sl][lane] = (sm->ss[sl][lane] & ~msk) | ((xbits << j0) & msk);
+            if (__any_sync(kFull, msk != 0u) && lane == 0) sm->prot_any |= 1u << sl;
         }
         // 2. decided_u (csfg_freeze.cpp:87)
-        scatter<q>(sm->dec_u, ubits, msk, start, sz);
+        scatter<q, W>(sm->dec_u, ubits, in_block, j0, start, sz);
         // 3. inactive-PE bookkeeping for stages after S (reference count rule)
-        if (start < frontier) {
-            if (lane < 32) sm->tmp[lane] = 0;
-            __syncwarp();
-            for (int r = start + lane; r < frontier; r += 32) {
-                const int fo = sm->fst[r];
-                for (int s2 = S + 1; s2 < M; ++s2)
-                    if (fo < s2 && !((r >> (M - 1 - s2)) & 1)) atomicAdd(&sm->tmp[s2], 1);
-            }
-            __syncwarp();
-            if (lane > S && lane < M) sm->inact[lane] += (sz >> 1) - sm->tmp[lane];
-        } else {
-            if (lane > S && lane < M) sm->inact[lane] += (sz >> 1);
-        }
-        for (int i = lane; i < sz; i += 32) sm->fst[start + i] = (uint8_t)S;
+        const int add = commit_counts<S>(start, sz);
+        inact_total += add;
         // 4. event log + frontier (csfg_freeze.cpp:88-92)
         if (lane == 0 && a->events && nev < a->ev_cap) {
             int* e = a->events + ((long long)frame_ * a->ev_cap + nev) * 5;
@@ -384,35 +494,63 @@ struct Dec {
         __syncwarp();
     }
 
-    long long frame_;
+    // updates inact[S+1 ..] and freeze_stage over the block; returns the
+    // increase of sum(inact)
+    template <int S>
+    __device__ __forceinline__ int commit_counts(int start, int sz) {
+        int add = 0;
+        if (start < frontier) {
+            sm->tmp[lane] = 0;
+            __syncwarp();
+#pragma unroll 1
+            for (int r = start + lane; r < frontier; r += 32) {
+                const int fo = sm->fst[r];
+#pragma unroll 1
+                for (int s2 = S + 1; s2 < M; ++s2)
+                    if (fo < s2 && !((r >> (M - 1 - s2)) & 1)) atomicAdd(&sm->tmp[s2], 1);
+            }
+            __syncwarp();
+            int v = 0;
+            if (lane > S && lane < M) {
+                v = (sz >> 1) - sm->tmp[lane];
+                sm->inact[lane] += v;
+            }
+            add = __reduce_add_sync(kFull, v);
+        } else {
+            if (lane > S && lane < M) sm->inact[lane] += (sz >> 1);
+            add = (M - 1 - S) * (sz >> 1);
+        }
+#pragma unroll 1
+        for (int i = lane; i < sz; i += 32) sm->fst[start + i] = (uint8_t)S;
+        return add;
+    }
 
-    // write `bits` (pass-q layout, rows selected by msk) into row-order words
-    template <int q>
-    __device__ __forceinline__ void scatter(uint32_t* words, uint32_t bits, uint32_t msk, int start,
+    // write the W block bits of this pass layout into row-order words
+    template <int q, int W>
+    __device__ __forceinline__ void scatter(uint32_t* words, uint32_t bits, bool in_block, int j0, int start,
                                             int sz) {
         constexpr int b = PL::base_bit(q);
         if constexpr (b == 5) {
             // row = lane + 32 j : word j collects bit j of every lane
-            const int j0 = start >> 5, j1 = (start + sz + 31) >> 5;
-            for (int j = j0; j < j1; ++j) {
-                const uint32_t w = __ballot_sync(kFull, (bits >> j) & 1u);
-                if (lane == 0) words[j] = w;
+#pragma unroll 1
+            for (int i = 0; i < W; ++i) {
+                const uint32_t w = __ballot_sync(kFull, (bits >> i) & 1u);
+                if (lane == 0) words[(start >> 5) + i] = w;
             }
         } else if constexpr (b == 0) {
             // row = P*lane + j : the block lives in one lane
-            if (msk) {
-                const int row0 = P * lane + (__ffs(msk) - 1);
+            if (in_block) {
+                const int row0 = P * lane + j0;
                 const int off = row0 & 31;
-                const uint32_t bm = (sz >= 32) ? 0xffffffffu : ((1u << sz) - 1u);
-                const uint32_t v = (bits >> (__ffs(msk) - 1)) & bm;
-                words[row0 >> 5] = (words[row0 >> 5] & ~(bm << off)) | (v << off);
+                const uint32_t bm = (W >= 32) ? 0xffffffffu : ((1u << W) - 1u);
+                words[row0 >> 5] = (words[row0 >> 5] & ~(bm << off)) | ((bits & bm) << off);
             }
         } else {
-#pragma unroll
-            for (int j = 0; j < P; ++j) {
-                if ((msk >> j) & 1u) {
-                    const int row = row_of<q>(j);
-                    if ((bits >> j) & 1u)
+            if (in_block) {
+#pragma unroll 1
+                for (int i = 0; i < W; ++i) {
+                    const int row = row_of<q>(j0 + i);
+                    if ((bits >> i) & 1u)
                         atomicOr(&words[row >> 5], 1u << (row & 31));
                     else
                         atomicAnd(&words[row >> 5], ~(1u << (row & 31)));
@@ -429,12 +567,17 @@ struct Dec {
         constexpr bool first_of_pass = (S == PL::first(q));
         constexpr bool last_of_pass = (S == PL::last(q));
         if constexpr (S == 0) {
-#pragma unroll
-            for (int j = 0; j < P; ++j) R[j] = sm->R0[row_of<0>(j)];
             if constexpr (KIND != 0) xq = 0u;
-        } else if constexpr (first_of_pass) {
 #pragma unroll
-            for (int j = 0; j < P; ++j) R[j] = sm->X[q - 1][xidx(row_of<q>(j))];
+            for (int c = 0; c < P / 4; ++c) {
+                const float4 v = sm->R0p[c][lane];
+                R[4 * c] = v.x;
+                R[4 * c + 1] = v.y;
+                R[4 * c + 2] = v.z;
+                R[4 * c + 3] = v.w;
+            }
+        } else if constexpr (first_of_pass) {
+            x_load<q>(sm->X[q - 1], R);
         }
         if constexpr (PL::is_boundary(S + 1)) {
             if constexpr (KIND == 2)
@@ -446,17 +589,17 @@ struct Dec {
         load_L<S + 1>(Lt);
         pe_stage<S>(Lt);
         store_L<S>(Lt);
-        if constexpr (last_of_pass && S + 1 < M) {
-#pragma unroll
-            for (int j = 0; j < P; ++j) sm->X[q][xidx(row_of<q>(j))] = R[j];
-        }
+        if constexpr (last_of_pass && S + 1 < M) x_store<q>(sm->X[q], R);
         if constexpr (first_of_pass || (last_of_pass && S + 1 < M)) __syncwarp();
         if constexpr (KIND == 2) {
-            act += (N >> 1) - sm->inact[S];
             check_commit<S>();
-            if (frontier >= N) return false;
-        } else {
-            act += (N >> 1);
+            if (frontier >= N) {
+                // reference stops the stage loop here: count stages 0..S only
+                int part = 0;
+                for (int s2 = 0; s2 <= S; ++s2) part += (N >> 1) - sm->inact[s2];
+                act += part;
+                return false;
+            }
         }
         return true;
     }
@@ -474,18 +617,16 @@ struct Dec {
     // the decided prefix [0, pin) taken from decided_u; returned as the
     // row-order word of this lane (lane < NW).
     __device__ __forceinline__ uint32_t u_words(int pin) {
-        uint32_t uq = 0u;
-#pragma unroll
-        for (int j = P - 1; j >= 0; --j) uq = __funnelshift_l(__float_as_uint(R[j]), uq, 1);
+        uint32_t uq = pack_range<0, P>();
         uq &= ~FZ[Q - 1];
         if (pin > 0) {
             const int r0 = P * lane;
             int cnt = pin - r0;
             cnt = cnt < 0 ? 0 : (cnt > P ? P : cnt);
-            const uint32_t pm = cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u);
+            const uint32_t pmk = cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u);
             const uint32_t pmask = P >= 32 ? 0xffffffffu : ((1u << P) - 1u);
             const uint32_t db = (sm->dec_u[r0 >> 5] >> (r0 & 31)) & pmask;
-            uq = (uq & ~pm) | (db & pm);
+            uq = (uq & ~pmk) | (db & pmk);
         }
         if constexpr (P == 32) {
             return uq;
@@ -509,8 +650,8 @@ struct Dec {
             const uint32_t o = __shfl_xor_sync(kFull, uw, h);
             if (!(lane & h)) uw ^= o;
         }
-        const uint32_t xw = transpose32(xq, lane);
-        return !__any_sync(kFull, (uw ^ xw) != 0u);
+        const uint32_t xw = __shfl_sync(kFull, transpose32(xq, lane), xperm);
+        return !__any_sync(kFull, lane < NW && uw != xw);
     }
 
     __device__ __forceinline__ void run(const DecodeArgs& args, WarpSmem<M>* s, int ln) {
@@ -518,12 +659,18 @@ struct Dec {
         sm = s;
         lane = ln;
         alpha = args.alpha;
-        // frozen rows per pass layout (fixed for the launch)
-#pragma unroll
-        for (int q = 0; q < Q; ++q) FZ[q] = 0u;
         fz_init<0>();
-        FZW = lane < NW ? args.frozen_bits[lane] : 0u;
-
+        // stage 0 pushes x_hat bits of rows (lane + 32 j) in the order
+        // j = j0, j0+1, j0+d, j0+d+1 for j0 = 0, 2, ... (d = P/2); the first push
+        // lands in bit 31. xperm = bit position that holds row-order word `lane`.
+        {
+            const int j = lane;
+            constexpr int d = P / 2;
+            const int hi = (j >= d) ? 1 : 0;
+            const int jj = j - hi * d;
+            const int p = 4 * (jj >> 1) + 2 * hi + (jj & 1);  // push index
+            xperm = P - 1 - p;
+        }
         if (lane < kNumCounters) sm->cnt[lane] = 0ull;
         __syncwarp();
 
@@ -533,21 +680,7 @@ struct Dec {
             f = __shfl_sync(kFull, f, 0);
             if (f >= args.frames) break;
             frame_ = f;
-            // ---- load LLRs (coalesced float4), bound check ----
-            const float4* src = reinterpret_cast<const float4*>(args.llr + f * (long long)N);
-            bool bad = false;
-#pragma unroll
-            for (int i = 0; i < P / 4; ++i) {
-                float4 v = __ldcs(src + lane + 32 * i);
-                bad |= !(fabsf(v.x) <= kClampFreeBound) | !(fabsf(v.y) <= kClampFreeBound) |
-                       !(fabsf(v.z) <= kClampFreeBound) | !(fabsf(v.w) <= kClampFreeBound);
-                v.x = __fadd_rn(v.x, 0.0f);
-                v.y = __fadd_rn(v.y, 0.0f);
-                v.z = __fadd_rn(v.z, 0.0f);
-                v.w = __fadd_rn(v.w, 0.0f);
-                reinterpret_cast<float4*>(sm->R0)[lane + 32 * i] = v;
-            }
-            if (__any_sync(kFull, bad)) {
+            if (!load_frame(f)) {
                 if (lane == 0) {
                     const unsigned long long slot = atomicAdd(args.list_len, 1ull);
                     args.list[slot] = f;
@@ -558,6 +691,7 @@ struct Dec {
             int iters = (KIND == 0) ? args.max_iter : 0;
             int stop = 0;
             bool converged = false;
+#pragma unroll 1
             for (int t = 1; t <= args.max_iter; ++t) {
                 if constexpr (KIND == 2) {
                     if (frontier >= N || converged) break;
@@ -565,6 +699,7 @@ struct Dec {
                 }
                 it = t;
                 const bool full = sweep_from<0>();
+                if (full) act += (long long)M * (N >> 1) - inact_total;
                 if constexpr (KIND == 1) {
                     if (gcheck(0)) {
                         iters = t;
@@ -588,43 +723,68 @@ struct Dec {
             } else {
                 uw = u_words(0);
             }
-            // ---- outputs ----
-            if (args.u_bits && lane < NW) args.u_bits[f * NW + lane] = uw;
-            if (lane == 0) {
-                if (args.iters) args.iters[f] = iters;
-                if (args.pe) args.pe[f] = act;
-                if (args.stop) args.stop[f] = (uint8_t)stop;
-                if (args.nev) args.nev[f] = nev;
-            }
-            if (args.counters) {
-                int be = 0;
-                if (lane < NW) be = __popc((uw ^ args.truth_u[f * NW + lane]) & ~FZW);
-                be = __reduce_add_sync(kFull, be);
-                unsigned long long v = 0ull;
-                switch (lane) {
-                    case kCntFrames: v = 1; break;
-                    case kCntBitErr: v = (unsigned long long)be; break;
-                    case kCntFrameErr: v = be > 0; break;
-                    case kCntIters: v = (unsigned long long)iters; break;
-                    case kCntItersSq: v = (unsigned long long)iters * iters; break;
-                    case kCntPe: v = (unsigned long long)act; break;
-                    case kCntEvents: v = (unsigned long long)nev; break;
-                    case kCntStop0: v = stop == 0; break;
-                    case kCntStop1: v = stop == 1; break;
-                    case kCntStop2: v = stop == 2; break;
-                    default: break;
-                }
-                if (lane < kNumCounters) sm->cnt[lane] += v;
-            }
+            write_outputs(f, uw, iters, stop);
         }
         if (args.counters && lane < kNumCounters && sm->cnt[lane])
             atomicAdd(&args.counters[lane], sm->cnt[lane]);
     }
 
+    __device__ __forceinline__ void write_outputs(long long f, uint32_t uw, int iters, int stop) {
+        const DecodeArgs& args = *a;
+        if (args.u_bits && lane < NW) args.u_bits[f * NW + lane] = uw;
+        if (lane == 0) {
+            if (args.iters) args.iters[f] = iters;
+            if (args.pe) args.pe[f] = act;
+            if (args.stop) args.stop[f] = (uint8_t)stop;
+            if (args.nev) args.nev[f] = nev;
+        }
+        if (args.counters) {
+            int be = 0;
+            if (lane < NW) be = __popc((uw ^ args.truth_u[f * NW + lane]) & ~args.frozen_bits[lane]);
+            be = __reduce_add_sync(kFull, be);
+            unsigned long long v = 0ull;
+            switch (lane) {
+                case kCntFrames: v = 1; break;
+                case kCntBitErr: v = (unsigned long long)be; break;
+                case kCntFrameErr: v = be > 0; break;
+                case kCntIters: v = (unsigned long long)iters; break;
+                case kCntItersSq: v = (unsigned long long)iters * iters; break;
+                case kCntPe: v = (unsigned long long)act; break;
+                case kCntEvents: v = (unsigned long long)nev; break;
+                case kCntStop0: v = stop == 0; break;
+                case kCntStop1: v = stop == 1; break;
+                case kCntStop2: v = stop == 2; break;
+                default: break;
+            }
+            if (lane < kNumCounters) sm->cnt[lane] += v;
+        }
+    }
+
+    // LLRs -> lane-private pass-0 layout; false when the frame needs the
+    // generic kernel (|LLR| beyond the clamp-free bound or non-finite)
+    __device__ __forceinline__ bool load_frame(long long f) {
+        const float4* src = reinterpret_cast<const float4*>(a->llr + f * (long long)N);
+        bool bad = false;
+        float* r0 = reinterpret_cast<float*>(sm->R0p);
+#pragma unroll 4
+        for (int i = 0; i < P / 4; ++i) {
+            const float4 v = __ldcs(src + lane + 32 * i);
+            const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                bad |= !(fabsf(e[k]) <= kClampFreeBound);
+                const int row = 4 * (lane + 32 * i) + k;  // row -> (lane', j) of pass 0
+                const int l2 = row & 31, j = row >> 5;
+                r0[((j >> 2) * 32 + l2) * 4 + (j & 3)] = __fadd_rn(e[k], 0.0f);  // -0 -> +0
+            }
+        }
+        return !__any_sync(kFull, bad);
+    }
+
     template <int q>
     __device__ __forceinline__ void fz_init() {
         uint32_t w = 0u;
-#pragma unroll
+#pragma unroll 1
         for (int j = 0; j < P; ++j) w |= (uint32_t)(a->frozen_rows[row_of<q>(j)] != 0) << j;
         FZ[q] = w;
         if constexpr (q + 1 < Q) fz_init<q + 1>();
@@ -632,41 +792,44 @@ struct Dec {
 
     __device__ __forceinline__ void init_frame() {
 #pragma unroll
-        for (int j = 0; j < P; ++j) R[j] = 0.f;
+        for (int j = 0; j < P; ++j) R[j] = 0.f;  // R(m) = 0 until the first sweep (max_iter = 0)
 #pragma unroll
-        for (int sl = 0; sl < PL::NLR; ++sl) {
-            PM[sl] = 0u;
-            SS[sl] = 0u;
+        for (int sl = 0; sl < PL::NLR; ++sl)
 #pragma unroll
             for (int j = 0; j < P; ++j) Lr[sl][j] = 0.f;
-        }
-#pragma unroll
-        for (int sl = 0; sl < PL::NLS; ++sl) {
-            PMW[sl] = 0u;
-#pragma unroll
+        init_smem();
+        frontier = 0;
+        nev = 0;
+        act = 0;
+        inact_total = 0;
+        xq = 0u;
+    }
+
+    __device__ __forceinline__ void init_smem() {
+#pragma unroll 1
+        for (int sl = 0; sl < PL::NLS; ++sl)
+#pragma unroll 1
             for (int c = 0; c < P / 4; ++c) sm->Ls[sl][c][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
+#pragma unroll 1
         for (int x = 0; x < Q - 1; ++x)
-#pragma unroll
-            for (int i = 0; i < P / 4; ++i)
-                reinterpret_cast<float4*>(sm->X[x])[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+            for (int i = lane; i < PL::NX; i += 32) sm->X[x][i] = 0.f;
+        // L(m): +CAP at frozen rows (bp_core.cpp:53), last-pass layout
         const uint32_t fl = FZ[Q - 1];
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < P / 4; ++c)
             sm->LM[c][lane] = make_float4(((fl >> (4 * c)) & 1u) ? kCap : 0.f, ((fl >> (4 * c + 1)) & 1u) ? kCap : 0.f,
                                           ((fl >> (4 * c + 2)) & 1u) ? kCap : 0.f, ((fl >> (4 * c + 3)) & 1u) ? kCap : 0.f);
         if (lane < NW) sm->dec_u[lane] = 0u;
-#pragma unroll
+#pragma unroll 1
         for (int x = 0; x < Q - 1; ++x)
             if (lane < NW) sm->xprot[x][lane] = 0u;
+#pragma unroll 1
+        for (int sl = 0; sl < PL::NLR + PL::NLS; ++sl) sm->pm[sl][lane] = 0u;
         sm->inact[lane] = 0;
-#pragma unroll
-        for (int i = 0; i < N / 128; ++i) reinterpret_cast<uint32_t*>(sm->fst)[lane + 32 * i] = 0x7f7f7f7fu;
-        frontier = 0;
-        nev = 0;
-        act = 0;
-        xq = 0u;
+        if (lane == 0) sm->prot_any = 0u;
+#pragma unroll 1
+        for (int i = lane; i < N / 4; i += 32) reinterpret_cast<uint32_t*>(sm->fst)[i] = 0x7f7f7f7fu;
         __syncwarp();
     }
 };
@@ -721,31 +884,29 @@ cudaError_t launch_warp(const DecodeArgs& a, int grid, cudaStream_t st) {
     return cudaErrorInvalidValue;
 }
 
-int warp_blocks_per_sm(int m, int kind) {
+template <int M, int KIND>
+static int occ_w() {
     int nb = 0;
-    const size_t smem = warp_smem_bytes(m);
-    cudaError_t e = cudaErrorInvalidValue;
-#define PBP_OCC(MM)                                                                               \
-    case MM:                                                                                      \
-        if (kind == 0) {                                                                          \
-            cudaFuncSetAttribute(wk::bp_warp_kernel<MM, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wk::bp_warp_kernel<MM, 0>, 32, smem); \
-        } else if (kind == 1) {                                                                   \
-            cudaFuncSetAttribute(wk::bp_warp_kernel<MM, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wk::bp_warp_kernel<MM, 1>, 32, smem); \
-        } else {                                                                                  \
-            cudaFuncSetAttribute(wk::bp_warp_kernel<MM, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wk::bp_warp_kernel<MM, 2>, 32, smem); \
-        }                                                                                         \
-        break;
+    const size_t smem = sizeof(wk::WarpSmem<M>);
+    cudaFuncSetAttribute(wk::bp_warp_kernel<M, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wk::bp_warp_kernel<M, KIND>, 32, smem) != cudaSuccess)
+        return 0;
+    return nb;
+}
+
+template <int M>
+static int occ_m(int kind) {
+    return kind == 0 ? occ_w<M, 0>() : kind == 1 ? occ_w<M, 1>() : occ_w<M, 2>();
+}
+
+int warp_blocks_per_sm(int m, int kind) {
     switch (m) {
-        PBP_OCC(7)
-        PBP_OCC(8)
-        PBP_OCC(9)
-        PBP_OCC(10)
+        case 7: return occ_m<7>(kind);
+        case 8: return occ_m<8>(kind);
+        case 9: return occ_m<9>(kind);
+        case 10: return occ_m<10>(kind);
     }
-#undef PBP_OCC
-    return e == cudaSuccess ? nb : 0;
+    return 0;
 }
 
 }  // namespace pbp
