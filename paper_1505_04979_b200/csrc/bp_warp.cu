@@ -42,6 +42,7 @@ namespace pbp {
 namespace wk {
 
 constexpr unsigned kFull = 0xffffffffu;
+__constant__ uint32_t c_jmask[5] = {0x55555555u, 0x33333333u, 0x0F0F0F0Fu, 0x00FF00FFu, 0x0000FFFFu};
 
 template <int M_>
 struct Plan {
@@ -107,7 +108,9 @@ struct WarpSmem {
     int inact[32];                         // inactive top rows per stage
     int tmp[32];
     unsigned long long cnt[16];            // per-warp counter accumulators
-    uint32_t prot_any;                     // bit per prot slot: some lane has a protected row
+    uint32_t sx[PL::M][32], su[PL::M][32]; // per stage: x_hat bits of R(s+1), block-transformed bits
+    uint32_t gviol[PL::M];                 // pass 0: groups with a violated frozen row
+    uint32_t fz[PL::Q][32];                // frozen rows per pass layout
     uint8_t fst[PL::N];                    // freeze_stage per row
 };
 
@@ -164,7 +167,8 @@ struct Dec {
     float Lr[PL::NLR][P];
     uint32_t FZ[Q];  // frozen rows per pass layout (bit j = row_of<q>(j))
 
-    int frontier, nev, it, inact_total;
+    int frontier, nev, it;
+    uint32_t prot;   // bit per protection slot: some lane holds a frozen-boundary row
     long long act, frame_;
     uint32_t xq;     // channel-side decisions of stage 0, permuted pass-0 layout
     int xperm;       // lane holding row-order word `lane` of x_hat after transpose
@@ -225,7 +229,7 @@ struct Dec {
             constexpr int sl = PL::reg_slot(T);
 #pragma unroll
             for (int j = 0; j < P; ++j) Lt[j] = Lr[sl][j];
-            if (sm->prot_any & (1u << sl)) {  // uniform, rare: boundary rows read as +-CAP
+            if (prot & (1u << sl)) {  // uniform, rare: boundary rows read as +-CAP
                 const uint32_t pm = sm->pm[sl][lane], ss = sm->ss[sl][lane];
 #pragma unroll
                 for (int j = 0; j < P; ++j)
@@ -258,7 +262,7 @@ struct Dec {
             constexpr int sl = PL::smem_slot(S);
             constexpr int ps = PL::prot_slot(S);
             constexpr int d = 1 << (M - 1 - S);  // last pass: b = 0
-            if (!(sm->prot_any & (1u << ps))) {
+            if (!(prot & (1u << ps))) {
 #pragma unroll
                 for (int c = 0; c < P / 4; ++c)
                     sm->Ls[sl][c][lane] = make_float4(Lt[4 * c], Lt[4 * c + 1], Lt[4 * c + 2], Lt[4 * c + 3]);
@@ -387,70 +391,108 @@ struct Dec {
         return v;
     }
 
-    template <int W, int G>
-    __device__ __forceinline__ uint32_t pack_block(int jb) const {
-        uint32_t v = 0u;
-#define PBP_CASE(i) \
-    case i:         \
-        if constexpr ((i) < G) v = pack_range<(i) * W, W>(); \
-        break;
-        switch (jb) {
-            PBP_CASE(0) PBP_CASE(1) PBP_CASE(2) PBP_CASE(3) PBP_CASE(4) PBP_CASE(5) PBP_CASE(6) PBP_CASE(7)
-            PBP_CASE(8) PBP_CASE(9) PBP_CASE(10) PBP_CASE(11) PBP_CASE(12) PBP_CASE(13) PBP_CASE(14) PBP_CASE(15)
-            PBP_CASE(16) PBP_CASE(17) PBP_CASE(18) PBP_CASE(19) PBP_CASE(20) PBP_CASE(21) PBP_CASE(22) PBP_CASE(23)
-            PBP_CASE(24) PBP_CASE(25) PBP_CASE(26) PBP_CASE(27) PBP_CASE(28) PBP_CASE(29) PBP_CASE(30) PBP_CASE(31)
-            default: break;
+    // sign bits of all P registers (bit j = R[j] < 0), four independent
+    // funnel-shift chains combined with PRMT (short dependency chain)
+    __device__ __forceinline__ uint32_t pack_all() const {
+        if constexpr (P >= 32) {
+            const uint32_t a0 = pack_range<0, 8>(), a1 = pack_range<8, 8>();
+            const uint32_t a2 = pack_range<16, 8>(), a3 = pack_range<24, 8>();
+            return __byte_perm(__byte_perm(a0, a1, 0x0040), __byte_perm(a2, a3, 0x0040), 0x5410);
+        } else if constexpr (P == 16) {
+            return __byte_perm(pack_range<0, 8>(), pack_range<8, 8>(), 0x0040) & 0xffffu;
+        } else {
+            return pack_range<0, P>();
         }
-#undef PBP_CASE
-        return v;
     }
 
-    // ---- csfg: candidate check + commit after stage S ------------------------
+    // ---- csfg: the candidate chain of one iteration -------------------------
+    // csfg_freeze.cpp:109-119 with the verified restructuring of SURVEY.md 0.9:
+    // the sweep computed every stage and snapshotted the sign bits of each
+    // R(s+1) (sm->snap); here the reference's stage loop is replayed in order -
+    // stop once the frontier covers n, count stage s's active PEs, check the
+    // block containing the frontier, commit - with the stage as a runtime value,
+    // so this code exists once. Exact because a stage-s commit only changes
+    // what later stages of the same sweep compute inside the frozen block
+    // (never read by an active PE or a later candidate) and L(s+1), which is
+    // next read in the following iteration.
+    static constexpr uint32_t mask_of(int which) {
+        uint32_t m = 0;
+        for (int x = 1; x <= M; ++x)
+            if ((which == 0 && PL::local_reg(x)) || (which == 1 && PL::local_smem(x))) m |= 1u << x;
+        return m;
+    }
+
+    // Sweep side of the check for stage S: x_hat = sign bits of R(S+1) and its
+    // polar transform inside every block-sized register group of every lane
+    // (all candidate positions at once, straight-line code). In pass 0 every
+    // block spans all lanes, so the lane-bit butterflies and the OR over lanes
+    // are done here too and one uniform word tells which groups satisfy every
+    // frozen row.
     template <int S>
-    __device__ __forceinline__ void check_commit() {
-        constexpr int q = PL::pass_of(S);
-        constexpr int b = PL::base_bit(q);
-        constexpr int g = M - 1 - S;       // log2 block size
-        constexpr int W = 1 << (g - b);    // registers per lane in a block
-        constexpr int hs = b + K - g;      // block-group bits within the lane
-        constexpr int G = 1 << hs;
-        const int bi = frontier >> g;
-        const int jb = bi & (G - 1);
-        const bool in_block = (lane >> b) == (bi >> hs);
-        const uint32_t xb = pack_block<W, G>(jb);
-        uint32_t u = xb;
-#pragma unroll
-        for (int gp = 0; gp < g; ++gp) {
-            if (gp >= b) {
-                const int tp = gp - b;
-                u ^= (u >> (1 << tp)) & jmask(tp);
-            } else {
-                const uint32_t o = __shfl_xor_sync(kFull, u, 1 << gp);
-                if (!((lane >> gp) & 1)) u ^= o;
-            }
-        }
-        constexpr uint32_t wmask = W >= 32 ? 0xffffffffu : ((1u << W) - 1u);
-        const uint32_t fzb = (FZ[q] >> (jb * W)) & wmask;
-        if (__any_sync(kFull, in_block && (u & fzb))) return;
-        commit<S, W>(bi, jb, in_block, xb & wmask, u & wmask);
-    }
-
-    template <int S, int W>
-    __device__ __forceinline__ void commit(int bi, int jb, bool in_block, uint32_t xbits, uint32_t ubits) {
+    __device__ __forceinline__ void snapshot() {
         constexpr int q = PL::pass_of(S);
         constexpr int b = PL::base_bit(q);
         constexpr int g = M - 1 - S;
-        constexpr int T = S + 1;
-        const int sz = 1 << g;
-        const int start = bi << g;
-        const int j0 = jb * W;
-        // 1. saturate / protect L(S+1) (csfg_freeze.cpp:84-86)
-        if constexpr (T == M || PL::local_smem(T)) {
-            float4* base;
-            if constexpr (T == M)
-                base = &sm->LM[0][0];
-            else
-                base = &sm->Ls[PL::smem_slot(T)][0][0];
+        const uint32_t xa = pack_all();
+        uint32_t u = xa;
+#pragma unroll
+        for (int tp = 0; tp < g - b; ++tp) u ^= (u >> (1 << tp)) & jmask(tp);
+#pragma unroll
+        for (int gp = 0; gp < (g < b ? g : b); ++gp) {
+            const uint32_t o = __shfl_xor_sync(kFull, u, 1 << gp);
+            if (!((lane >> gp) & 1)) u ^= o;
+        }
+        if constexpr (b == 5) {
+            const uint32_t vw = __reduce_or_sync(kFull, u & FZ[q]);
+            if (lane == 0) sm->gviol[S] = vw;
+        }
+        sm->sx[S][lane] = xa;
+        sm->su[S][lane] = u;
+    }
+
+    // returns frontier < n (the reference then runs the pinned G-check)
+    __device__ __forceinline__ bool chain() {
+        __syncwarp();  // snapshots of the whole warp
+#pragma unroll 1
+        for (int s = 0; s < M; ++s) {
+            if (frontier >= N) break;
+            act += (N >> 1) - sm->inact[s];  // stage_pass count under the current freeze state
+            const int q = s / K;
+            const int b = (M - K - q * K) > 0 ? (M - K - q * K) : 0;
+            const int g = M - 1 - s;
+            const int W = 1 << (g - b);
+            const int hs = b + K - g;
+            const int bi = frontier >> g;
+            const int j0 = (bi & ((1 << hs) - 1)) * W;
+            const int bl = bi >> hs;  // lane_hi of the block
+            const bool in_block = (lane >> b) == bl;
+            const uint32_t wm = W >= 32 ? 0xffffffffu : ((1u << W) - 1u);
+            uint32_t vw;
+            if (b == 5) {
+                vw = sm->gviol[s];                         // precomputed in the sweep
+            } else if (b == 0) {
+                vw = sm->su[s][bl] & sm->fz[q][bl];        // the block lives in lane bl
+            } else {
+                vw = __reduce_or_sync(kFull, in_block ? (sm->su[s][lane] & sm->fz[q][lane]) : 0u);
+            }
+            if ((vw >> j0) & wm) continue;
+            commit(s, bi, b, q, W, j0, in_block, (sm->sx[s][lane] >> j0) & wm, (sm->su[s][lane] >> j0) & wm);
+        }
+        return frontier < N;
+    }
+
+    // apply_freeze (csfg_freeze.cpp:82-93): saturate/protect L(S+1), decided_u,
+    // freeze_stage + inactive-PE counts, freeze-event log, frontier.
+    __device__ __forceinline__ void commit(int S, int bi, int b, int q, int W, int j0, bool in_block,
+                                           uint32_t xbits, uint32_t ubits) {
+        constexpr uint32_t REGM = mask_of(0), SMEMM = mask_of(1);
+        const int g = M - 1 - S;
+        const int sz = 1 << g, start = bi << g;
+        const uint32_t wm = W >= 32 ? 0xffffffffu : ((1u << W) - 1u);
+        const uint32_t msk = in_block ? (wm << j0) : 0u;
+        const int T = S + 1;
+        if (T == M || ((SMEMM >> T) & 1u)) {
+            float4* base = (T == M) ? &sm->LM[0][0] : &sm->Ls[__popc(SMEMM & ((1u << T) - 1u))][0][0];
             if (in_block) {
 #pragma unroll 1
                 for (int i = 0; i < W; ++i) {
@@ -458,29 +500,22 @@ struct Dec {
                     reinterpret_cast<float*>(&base[(j >> 2) * 32 + lane])[j & 3] = ((xbits >> i) & 1u) ? -kCap : kCap;
                 }
             }
-            if constexpr (T != M) {
-                constexpr int ps = PL::prot_slot(T);
-                const uint32_t msk = in_block ? (((W >= 32) ? 0xffffffffu : ((1u << W) - 1u)) << j0) : 0u;
+            if (T != M) {
+                const int ps = PL::NLR + __popc(SMEMM & ((1u << T) - 1u));
                 sm->pm[ps][lane] |= msk;
-                if (__any_sync(kFull, msk != 0u) && lane == 0) sm->prot_any |= 1u << ps;
+                if (__any_sync(kFull, msk != 0u)) prot |= 1u << ps;
             }
-        } else if constexpr (PL::is_boundary(T)) {
-            constexpr int qb = PL::pass_of(T);
-            if (lane == 0) sm->xprot[qb - 1][bi >> 5] |= 1u << (bi & 31);
-            scatter<q, W>(sm->sat, xbits, in_block, j0, start, sz);
-        } else {
-            constexpr int sl = PL::reg_slot(T);
-            const uint32_t msk = in_block ? (((W >= 32) ? 0xffffffffu : ((1u << W) - 1u)) << j0) : 0u;
+        } else if ((REGM >> T) & 1u) {
+            const int sl = __popc(REGM & ((1u << T) - 1u));
             sm->pm[sl][lane] |= msk;
             sm->ss[sl][lane] = (sm->ss[sl][lane] & ~msk) | ((xbits << j0) & msk);
-            if (__any_sync(kFull, msk != 0u) && lane == 0) sm->prot_any |= 1u << sl;
+            if (__any_sync(kFull, msk != 0u)) prot |= 1u << sl;
+        } else {  // pass boundary: re-saturated before its next read
+            if (lane == 0) sm->xprot[T / K - 1][bi >> 5] |= 1u << (bi & 31);
+            scatter(sm->sat, xbits, in_block, b, q, W, j0, start);
         }
-        // 2. decided_u (csfg_freeze.cpp:87)
-        scatter<q, W>(sm->dec_u, ubits, in_block, j0, start, sz);
-        // 3. inactive-PE bookkeeping for stages after S (reference count rule)
-        const int add = commit_counts<S>(start, sz);
-        inact_total += add;
-        // 4. event log + frontier (csfg_freeze.cpp:88-92)
+        scatter(sm->dec_u, ubits, in_block, b, q, W, j0, start);
+        commit_counts(S, start, sz, frontier);
         if (lane == 0 && a->events && nev < a->ev_cap) {
             int* e = a->events + ((long long)frame_ * a->ev_cap + nev) * 5;
             e[0] = it;
@@ -494,16 +529,16 @@ struct Dec {
         __syncwarp();
     }
 
-    // updates inact[S+1 ..] and freeze_stage over the block; returns the
-    // increase of sum(inact)
-    template <int S>
-    __device__ __forceinline__ int commit_counts(int start, int sz) {
-        int add = 0;
-        if (start < frontier) {
+    // inact[S+1 ..] and freeze_stage over the block [start, start+sz); rows of
+    // [start, fr0) were decided earlier (an enclosing block supersedes them).
+    // Returns the increase of sum(inact).
+    __device__ __forceinline__ int commit_counts(int S, int start, int sz, int fr0) {  // returns added inactive rows
+        int add;
+        if (start < fr0) {
             sm->tmp[lane] = 0;
             __syncwarp();
 #pragma unroll 1
-            for (int r = start + lane; r < frontier; r += 32) {
+            for (int r = start + lane; r < fr0; r += 32) {
                 const int fo = sm->fst[r];
 #pragma unroll 1
                 for (int s2 = S + 1; s2 < M; ++s2)
@@ -522,22 +557,21 @@ struct Dec {
         }
 #pragma unroll 1
         for (int i = lane; i < sz; i += 32) sm->fst[start + i] = (uint8_t)S;
+        __syncwarp();
         return add;
     }
 
-    // write the W block bits of this pass layout into row-order words
-    template <int q, int W>
-    __device__ __forceinline__ void scatter(uint32_t* words, uint32_t bits, bool in_block, int j0, int start,
-                                            int sz) {
-        constexpr int b = PL::base_bit(q);
-        if constexpr (b == 5) {
+    // write W block bits of a pass layout (base bit b) into row-order words
+    __device__ __forceinline__ void scatter(uint32_t* words, uint32_t bits, bool in_block, int b, int q, int W,
+                                            int j0, int start) {
+        if (b == 5) {
             // row = lane + 32 j : word j collects bit j of every lane
 #pragma unroll 1
             for (int i = 0; i < W; ++i) {
                 const uint32_t w = __ballot_sync(kFull, (bits >> i) & 1u);
                 if (lane == 0) words[(start >> 5) + i] = w;
             }
-        } else if constexpr (b == 0) {
+        } else if (b == 0) {
             // row = P*lane + j : the block lives in one lane
             if (in_block) {
                 const int row0 = P * lane + j0;
@@ -545,16 +579,15 @@ struct Dec {
                 const uint32_t bm = (W >= 32) ? 0xffffffffu : ((1u << W) - 1u);
                 words[row0 >> 5] = (words[row0 >> 5] & ~(bm << off)) | ((bits & bm) << off);
             }
-        } else {
-            if (in_block) {
+        } else if (in_block) {
 #pragma unroll 1
-                for (int i = 0; i < W; ++i) {
-                    const int row = row_of<q>(j0 + i);
-                    if ((bits >> i) & 1u)
-                        atomicOr(&words[row >> 5], 1u << (row & 31));
-                    else
-                        atomicAnd(&words[row >> 5], ~(1u << (row & 31)));
-                }
+            for (int i = 0; i < W; ++i) {
+                const int j = j0 + i;
+                const int row = (lane & ((1 << b) - 1)) | (j << b) | ((lane >> b) << (b + K));
+                if ((bits >> i) & 1u)
+                    atomicOr(&words[row >> 5], 1u << (row & 31));
+                else
+                    atomicAnd(&words[row >> 5], ~(1u << (row & 31)));
             }
         }
         __syncwarp();
@@ -591,16 +624,7 @@ struct Dec {
         store_L<S>(Lt);
         if constexpr (last_of_pass && S + 1 < M) x_store<q>(sm->X[q], R);
         if constexpr (first_of_pass || (last_of_pass && S + 1 < M)) __syncwarp();
-        if constexpr (KIND == 2) {
-            check_commit<S>();
-            if (frontier >= N) {
-                // reference stops the stage loop here: count stages 0..S only
-                int part = 0;
-                for (int s2 = 0; s2 <= S; ++s2) part += (N >> 1) - sm->inact[s2];
-                act += part;
-                return false;
-            }
-        }
+        if constexpr (KIND == 2) snapshot<S>();
         return true;
     }
 
@@ -617,7 +641,7 @@ struct Dec {
     // the decided prefix [0, pin) taken from decided_u; returned as the
     // row-order word of this lane (lane < NW).
     __device__ __forceinline__ uint32_t u_words(int pin) {
-        uint32_t uq = pack_range<0, P>();
+        uint32_t uq = pack_all();
         uq &= ~FZ[Q - 1];
         if (pin > 0) {
             const int r0 = P * lane;
@@ -698,16 +722,18 @@ struct Dec {
                     iters = t;
                 }
                 it = t;
-                const bool full = sweep_from<0>();
-                if (full) act += (long long)M * (N >> 1) - inact_total;
+                sweep_from<0>();
+                if constexpr (KIND == 2) {
+                    if (chain()) converged = gcheck(frontier);
+                } else {
+                    act += (long long)M * (N >> 1);
+                }
                 if constexpr (KIND == 1) {
                     if (gcheck(0)) {
                         iters = t;
                         stop = 1;
                         break;
                     }
-                } else if constexpr (KIND == 2) {
-                    if (full && frontier < N) converged = gcheck(frontier);
                 }
             }
             if constexpr (KIND == 1) {
@@ -787,6 +813,7 @@ struct Dec {
 #pragma unroll 1
         for (int j = 0; j < P; ++j) w |= (uint32_t)(a->frozen_rows[row_of<q>(j)] != 0) << j;
         FZ[q] = w;
+        sm->fz[q][lane] = w;
         if constexpr (q + 1 < Q) fz_init<q + 1>();
     }
 
@@ -801,7 +828,7 @@ struct Dec {
         frontier = 0;
         nev = 0;
         act = 0;
-        inact_total = 0;
+        prot = 0u;
         xq = 0u;
     }
 
@@ -827,7 +854,6 @@ struct Dec {
 #pragma unroll 1
         for (int sl = 0; sl < PL::NLR + PL::NLS; ++sl) sm->pm[sl][lane] = 0u;
         sm->inact[lane] = 0;
-        if (lane == 0) sm->prot_any = 0u;
 #pragma unroll 1
         for (int i = lane; i < N / 4; i += 32) reinterpret_cast<uint32_t*>(sm->fst)[i] = 0x7f7f7f7fu;
         __syncwarp();

