@@ -80,6 +80,7 @@ SIGNATURES = {
                                           C.POINTER(C.c_int64), _P]),
     "pbp_kernel_path": (C.c_int, [C.c_int32]),
     "pbp_ctx_force_generic": (C.c_int, [_P, C.c_int]),
+    "pbp_kernel_info": (C.c_int, [C.c_int32, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "pbp_last_launch_info": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
 }
 
@@ -88,7 +89,7 @@ def load(path: str = LIB_PATH):
     """Load libpbp.so. Raises (no fallback) when the extension has not been built."""
     if not os.path.exists(path):
         raise ImportError(
-            f"libpbp.so not found at {path}: build it with `python -m paper_1505_04979_b200.build` "
+            f"libpbp.so not found at {path}: build it with `python paper_1505_04979_b200/build.py` "
             "(there is no CPU fallback)")
     lib = C.CDLL(path)
     for name, (res, args) in SIGNATURES.items():

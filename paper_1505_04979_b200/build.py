@@ -1,6 +1,7 @@
 """In-tree build of libpbp.so (CUDA kernels for sm_100a + C ABI + C++ host API).
 
-Run as ``python -m paper_1505_04979_b200.build`` or via ``__graft_entry__.build()``.
+Run as ``python paper_1505_04979_b200/build.py`` or via ``__graft_entry__.build()`` (not with
+``-m``: importing the package loads the library it builds).
 Objects go to build/, the shared library to paper_1505_04979_b200/_lib/ so it
 travels to the GPU box with the repo snapshot.
 """

@@ -99,7 +99,7 @@ struct WarpSmem {
     float4 R0p[PL::P / 4][32];             // channel LLRs, lane-private pass-0 layout
     float X[PL::Q - 1][PL::NX];            // pass boundaries: R(e) then L(e), padded rows
     float4 Ls[PL::NLS][PL::P / 4][32];     // lane-private L slots (last pass, n=1024)
-    float4 LM[PL::P / 4][32];              // L(m), lane-private, last-pass layout
+    uint32_t lmz[32], lms[32];             // L(m) in {0,+-CAP}: nonzero / negative rows, last-pass layout
     uint32_t pm[PL::NLR + PL::NLS][32];    // per lane: rows whose L(s) is a frozen boundary
     uint32_t ss[PL::NLR][32];              // ... and their signs (register arrays)
     uint32_t dec_u[PL::NW];                // decided_u bits (row order)
@@ -108,7 +108,7 @@ struct WarpSmem {
     int inact[32];                         // inactive top rows per stage
     int tmp[32];
     unsigned long long cnt[16];            // per-warp counter accumulators
-    uint32_t sx[PL::M][32], su[PL::M][32]; // per stage: x_hat bits of R(s+1), block-transformed bits
+    uint32_t su[PL::M][32];                // per stage: block-transformed sign bits of R(s+1)
     uint32_t gviol[PL::M];                 // pass 0: groups with a violated frozen row
     uint32_t fz[PL::Q][32];                // frozen rows per pass layout
     uint8_t fst[PL::N];                    // freeze_stage per row
@@ -215,14 +215,10 @@ struct Dec {
     __device__ __forceinline__ void load_L(float (&Lt)[P]) {
         constexpr int q = PL::pass_of(T - 1);
         if constexpr (T == M) {
+            // L(m) (bp_core.cpp:53, csfg_freeze.cpp:86) only takes 0, +CAP, -CAP
+            const uint32_t nz = sm->lmz[lane], ng = sm->lms[lane];
 #pragma unroll
-            for (int c = 0; c < P / 4; ++c) {
-                const float4 v = sm->LM[c][lane];
-                Lt[4 * c] = v.x;
-                Lt[4 * c + 1] = v.y;
-                Lt[4 * c + 2] = v.z;
-                Lt[4 * c + 3] = v.w;
-            }
+            for (int j = 0; j < P; ++j) Lt[j] = ((nz >> j) & 1u) ? (((ng >> j) & 1u) ? -kCap : kCap) : 0.f;
         } else if constexpr (PL::is_boundary(T)) {
             x_load<q>(sm->X[PL::pass_of(T) - 1], Lt);
         } else if constexpr (PL::local_reg(T)) {
@@ -433,8 +429,7 @@ struct Dec {
         constexpr int q = PL::pass_of(S);
         constexpr int b = PL::base_bit(q);
         constexpr int g = M - 1 - S;
-        const uint32_t xa = pack_all();
-        uint32_t u = xa;
+        uint32_t u = pack_all();
 #pragma unroll
         for (int tp = 0; tp < g - b; ++tp) u ^= (u >> (1 << tp)) & jmask(tp);
 #pragma unroll
@@ -446,7 +441,6 @@ struct Dec {
             const uint32_t vw = __reduce_or_sync(kFull, u & FZ[q]);
             if (lane == 0) sm->gviol[S] = vw;
         }
-        sm->sx[S][lane] = xa;
         sm->su[S][lane] = u;
     }
 
@@ -476,7 +470,17 @@ struct Dec {
                 vw = __reduce_or_sync(kFull, in_block ? (sm->su[s][lane] & sm->fz[q][lane]) : 0u);
             }
             if ((vw >> j0) & wm) continue;
-            commit(s, bi, b, q, W, j0, in_block, (sm->sx[s][lane] >> j0) & wm, (sm->su[s][lane] >> j0) & wm);
+            // x_hat = T(u_hat): the block transform is an involution (polar_code.hpp:17-19)
+            const uint32_t uu = sm->su[s][lane];
+            uint32_t xx = uu;
+#pragma unroll 1
+            for (int tp = 0; tp < g - b; ++tp) xx ^= (xx >> (1 << tp)) & c_jmask[tp];
+#pragma unroll 1
+            for (int gp = 0; gp < (g < b ? g : b); ++gp) {
+                const uint32_t o = __shfl_xor_sync(kFull, xx, 1 << gp);
+                if (!((lane >> gp) & 1)) xx ^= o;
+            }
+            commit(s, bi, b, q, W, j0, in_block, (xx >> j0) & wm, (uu >> j0) & wm);
         }
         return frontier < N;
     }
@@ -491,8 +495,11 @@ struct Dec {
         const uint32_t wm = W >= 32 ? 0xffffffffu : ((1u << W) - 1u);
         const uint32_t msk = in_block ? (wm << j0) : 0u;
         const int T = S + 1;
-        if (T == M || ((SMEMM >> T) & 1u)) {
-            float4* base = (T == M) ? &sm->LM[0][0] : &sm->Ls[__popc(SMEMM & ((1u << T) - 1u))][0][0];
+        if (T == M) {
+            sm->lmz[lane] |= msk;
+            sm->lms[lane] = (sm->lms[lane] & ~msk) | ((xbits << j0) & msk);
+        } else if ((SMEMM >> T) & 1u) {
+            float4* base = &sm->Ls[__popc(SMEMM & ((1u << T) - 1u))][0][0];
             if (in_block) {
 #pragma unroll 1
                 for (int i = 0; i < W; ++i) {
@@ -500,11 +507,9 @@ struct Dec {
                     reinterpret_cast<float*>(&base[(j >> 2) * 32 + lane])[j & 3] = ((xbits >> i) & 1u) ? -kCap : kCap;
                 }
             }
-            if (T != M) {
-                const int ps = PL::NLR + __popc(SMEMM & ((1u << T) - 1u));
-                sm->pm[ps][lane] |= msk;
-                if (__any_sync(kFull, msk != 0u)) prot |= 1u << ps;
-            }
+            const int ps = PL::NLR + __popc(SMEMM & ((1u << T) - 1u));
+            sm->pm[ps][lane] |= msk;
+            if (__any_sync(kFull, msk != 0u)) prot |= 1u << ps;
         } else if ((REGM >> T) & 1u) {
             const int sl = __popc(REGM & ((1u << T) - 1u));
             sm->pm[sl][lane] |= msk;
@@ -842,11 +847,8 @@ struct Dec {
 #pragma unroll 1
             for (int i = lane; i < PL::NX; i += 32) sm->X[x][i] = 0.f;
         // L(m): +CAP at frozen rows (bp_core.cpp:53), last-pass layout
-        const uint32_t fl = FZ[Q - 1];
-#pragma unroll 1
-        for (int c = 0; c < P / 4; ++c)
-            sm->LM[c][lane] = make_float4(((fl >> (4 * c)) & 1u) ? kCap : 0.f, ((fl >> (4 * c + 1)) & 1u) ? kCap : 0.f,
-                                          ((fl >> (4 * c + 2)) & 1u) ? kCap : 0.f, ((fl >> (4 * c + 3)) & 1u) ? kCap : 0.f);
+        sm->lmz[lane] = FZ[Q - 1];
+        sm->lms[lane] = 0u;
         if (lane < NW) sm->dec_u[lane] = 0u;
 #pragma unroll 1
         for (int x = 0; x < Q - 1; ++x)
