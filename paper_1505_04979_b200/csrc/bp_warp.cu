@@ -99,7 +99,7 @@ struct WarpSmem {
     float4 R0p[PL::P / 4][32];             // channel LLRs, lane-private pass-0 layout
     float X[PL::Q - 1][PL::NX];            // pass boundaries: R(e) then L(e), padded rows
     float4 Ls[PL::NLS][PL::P / 4][32];     // lane-private L slots (last pass, n=1024)
-    uint32_t lmz[32], lms[32];             // L(m) in {0,+-CAP}: nonzero / negative rows, last-pass layout
+    float4 LM[PL::P / 4][32];              // L(m), lane-private, last-pass layout
     uint32_t pm[PL::NLR + PL::NLS][32];    // per lane: rows whose L(s) is a frozen boundary
     uint32_t ss[PL::NLR][32];              // ... and their signs (register arrays)
     uint32_t dec_u[PL::NW];                // decided_u bits (row order)
@@ -109,7 +109,8 @@ struct WarpSmem {
     int tmp[32];
     unsigned long long cnt[16];            // per-warp counter accumulators
     uint32_t su[PL::M][32];                // per stage: block-transformed sign bits of R(s+1)
-    uint32_t gviol[PL::M];                 // pass 0: groups with a violated frozen row
+    uint32_t sv[PL::M][32];                // per stage: violated groups, OR over a block's lanes
+    int cS[PL::M], cbi[PL::M];             // commits recorded by the walk of one iteration
     uint32_t fz[PL::Q][32];                // frozen rows per pass layout
     uint8_t fst[PL::N];                    // freeze_stage per row
 };
@@ -215,10 +216,14 @@ struct Dec {
     __device__ __forceinline__ void load_L(float (&Lt)[P]) {
         constexpr int q = PL::pass_of(T - 1);
         if constexpr (T == M) {
-            // L(m) (bp_core.cpp:53, csfg_freeze.cpp:86) only takes 0, +CAP, -CAP
-            const uint32_t nz = sm->lmz[lane], ng = sm->lms[lane];
 #pragma unroll
-            for (int j = 0; j < P; ++j) Lt[j] = ((nz >> j) & 1u) ? (((ng >> j) & 1u) ? -kCap : kCap) : 0.f;
+            for (int c = 0; c < P / 4; ++c) {
+                const float4 v = sm->LM[c][lane];
+                Lt[4 * c] = v.x;
+                Lt[4 * c + 1] = v.y;
+                Lt[4 * c + 2] = v.z;
+                Lt[4 * c + 3] = v.w;
+            }
         } else if constexpr (PL::is_boundary(T)) {
             x_load<q>(sm->X[PL::pass_of(T) - 1], Lt);
         } else if constexpr (PL::local_reg(T)) {
@@ -420,10 +425,9 @@ struct Dec {
 
     // Sweep side of the check for stage S: x_hat = sign bits of R(S+1) and its
     // polar transform inside every block-sized register group of every lane
-    // (all candidate positions at once, straight-line code). In pass 0 every
-    // block spans all lanes, so the lane-bit butterflies and the OR over lanes
-    // are done here too and one uniform word tells which groups satisfy every
-    // frozen row.
+    // (all candidate positions at once, straight-line code), then the frozen-row
+    // violations OR-ed over the lanes a block spans (its lane_lo bits): sv[S][l]
+    // tells, for the lane group of l, which register groups would be rejected.
     template <int S>
     __device__ __forceinline__ void snapshot() {
         constexpr int q = PL::pass_of(S);
@@ -437,41 +441,96 @@ struct Dec {
             const uint32_t o = __shfl_xor_sync(kFull, u, 1 << gp);
             if (!((lane >> gp) & 1)) u ^= o;
         }
+        uint32_t v = u & FZ[q];
         if constexpr (b == 5) {
-            const uint32_t vw = __reduce_or_sync(kFull, u & FZ[q]);
-            if (lane == 0) sm->gviol[S] = vw;
+            v = __reduce_or_sync(kFull, v);
+        } else {
+#pragma unroll
+            for (int gp = 0; gp < b; ++gp) v |= __shfl_xor_sync(kFull, v, 1 << gp);
         }
+        sm->sv[S][lane] = v;
         sm->su[S][lane] = u;
     }
 
-    // returns frontier < n (the reference then runs the pinned G-check)
+    // The reference's stage loop (csfg_freeze.cpp:109-119) replayed after the
+    // sweep, in two phases. (1) Walk: between two commits the frontier is
+    // fixed, so lane s evaluates stage s's candidate for the current frontier
+    // and one ballot finds the first accepting stage; stages before it reject,
+    // it commits, the frontier moves, the rest are evaluated again. Only the
+    // frontier is needed for that. (2) The side effects of the recorded commits
+    // (apply_freeze) in order, with one trailing __syncwarp. Returns
+    // frontier < n (the reference then runs the pinned G-check).
     __device__ __forceinline__ bool chain() {
+#ifdef PBP_DBG_NOCHAIN  // timing experiments only: results are wrong
+        act += (long long)M * (N >> 1);
+        return frontier < N;
+#endif
         __syncwarp();  // snapshots of the whole warp
+        int s_next = 0, s_last = M - 1, nc = 0;
+        const int fr_start = frontier;
+        bool done = false;
 #pragma unroll 1
-        for (int s = 0; s < M; ++s) {
-            if (frontier >= N) break;
-            act += (N >> 1) - sm->inact[s];  // stage_pass count under the current freeze state
-            const int q = s / K;
+        while (s_next < M) {
+            bool acc = false;
+            if (lane >= s_next && lane < M) {
+                const int st = lane;
+                const int q = st / K;
+                const int b = (M - K - q * K) > 0 ? (M - K - q * K) : 0;
+                const int g = M - 1 - st;
+                const int W = 1 << (g - b);
+                const int hs = b + K - g;
+                const int bi = frontier >> g;
+                const int j0 = (bi & ((1 << hs) - 1)) * W;
+                const uint32_t wm = W >= 32 ? 0xffffffffu : ((1u << W) - 1u);
+                acc = ((sm->sv[st][(bi >> hs) << b] >> j0) & wm) == 0u;
+            }
+            const uint32_t am = __ballot_sync(kFull, acc);
+            if (!am) break;
+            const int st = __ffs(am) - 1;
+            const int g = M - 1 - st;
+            if (lane == 0) {
+                sm->cS[nc] = st;
+                sm->cbi[nc] = frontier >> g;
+            }
+            ++nc;
+            frontier = ((frontier >> g) + 1) << g;
+            if (frontier >= N) {
+                s_last = st;
+                done = true;
+                break;
+            }
+            s_next = st + 1;
+        }
+        if (nc) apply_commits(nc, fr_start);
+        // stage_pass counts of stages 0..s_last under the freeze state each ran
+        // with (a commit at stage s only changes inact[s' > s])
+        const int v = lane <= s_last ? (N >> 1) - sm->inact[lane] : 0;
+        act += __reduce_add_sync(kFull, v);
+        return !done;
+    }
+
+    // apply_freeze (csfg_freeze.cpp:82-93) for the commits of one iteration,
+    // in order: saturate/protect L(S+1), decided_u, inactive-PE counts,
+    // freeze_stage, event log.
+    __device__ __forceinline__ void apply_commits(int nc, int fr_start) {
+        constexpr uint32_t REGM = mask_of(0), SMEMM = mask_of(1);
+        __syncwarp();
+        int dinact = 0;  // this lane's stage: newly inactive top rows
+#pragma unroll 1
+        for (int k = 0; k < nc; ++k) {
+            const int S = sm->cS[k], bi = sm->cbi[k];
+            const int q = S / K;
             const int b = (M - K - q * K) > 0 ? (M - K - q * K) : 0;
-            const int g = M - 1 - s;
+            const int g = M - 1 - S;
             const int W = 1 << (g - b);
             const int hs = b + K - g;
-            const int bi = frontier >> g;
             const int j0 = (bi & ((1 << hs) - 1)) * W;
-            const int bl = bi >> hs;  // lane_hi of the block
-            const bool in_block = (lane >> b) == bl;
+            const bool in_block = (lane >> b) == (bi >> hs);
             const uint32_t wm = W >= 32 ? 0xffffffffu : ((1u << W) - 1u);
-            uint32_t vw;
-            if (b == 5) {
-                vw = sm->gviol[s];                         // precomputed in the sweep
-            } else if (b == 0) {
-                vw = sm->su[s][bl] & sm->fz[q][bl];        // the block lives in lane bl
-            } else {
-                vw = __reduce_or_sync(kFull, in_block ? (sm->su[s][lane] & sm->fz[q][lane]) : 0u);
-            }
-            if ((vw >> j0) & wm) continue;
-            // x_hat = T(u_hat): the block transform is an involution (polar_code.hpp:17-19)
-            const uint32_t uu = sm->su[s][lane];
+            const uint32_t msk = in_block ? (wm << j0) : 0u;
+            const int sz = 1 << g, start = bi << g;
+            // u_hat of the block; x_hat = T(u_hat) (the transform is an involution)
+            const uint32_t uu = sm->su[S][lane];
             uint32_t xx = uu;
 #pragma unroll 1
             for (int tp = 0; tp < g - b; ++tp) xx ^= (xx >> (1 << tp)) & c_jmask[tp];
@@ -480,90 +539,83 @@ struct Dec {
                 const uint32_t o = __shfl_xor_sync(kFull, xx, 1 << gp);
                 if (!((lane >> gp) & 1)) xx ^= o;
             }
-            commit(s, bi, b, q, W, j0, in_block, (xx >> j0) & wm, (uu >> j0) & wm);
-        }
-        return frontier < N;
-    }
-
-    // apply_freeze (csfg_freeze.cpp:82-93): saturate/protect L(S+1), decided_u,
-    // freeze_stage + inactive-PE counts, freeze-event log, frontier.
-    __device__ __forceinline__ void commit(int S, int bi, int b, int q, int W, int j0, bool in_block,
-                                           uint32_t xbits, uint32_t ubits) {
-        constexpr uint32_t REGM = mask_of(0), SMEMM = mask_of(1);
-        const int g = M - 1 - S;
-        const int sz = 1 << g, start = bi << g;
-        const uint32_t wm = W >= 32 ? 0xffffffffu : ((1u << W) - 1u);
-        const uint32_t msk = in_block ? (wm << j0) : 0u;
-        const int T = S + 1;
-        if (T == M) {
-            sm->lmz[lane] |= msk;
-            sm->lms[lane] = (sm->lms[lane] & ~msk) | ((xbits << j0) & msk);
-        } else if ((SMEMM >> T) & 1u) {
-            float4* base = &sm->Ls[__popc(SMEMM & ((1u << T) - 1u))][0][0];
-            if (in_block) {
+            const uint32_t xbits = (xx >> j0) & wm, ubits = (uu >> j0) & wm;
+            // 1. saturate / protect L(S+1) (csfg_freeze.cpp:84-86)
+            const int T = S + 1;
+            if (T == M || ((SMEMM >> T) & 1u)) {
+                float4* base = (T == M) ? &sm->LM[0][0] : &sm->Ls[__popc(SMEMM & ((1u << T) - 1u))][0][0];
+                if (in_block) {
+                    if (W >= 4) {
 #pragma unroll 1
-                for (int i = 0; i < W; ++i) {
-                    const int j = j0 + i;
-                    reinterpret_cast<float*>(&base[(j >> 2) * 32 + lane])[j & 3] = ((xbits >> i) & 1u) ? -kCap : kCap;
+                        for (int i = 0; i < W; i += 4)
+                            base[((j0 + i) >> 2) * 32 + lane] = make_float4(
+                                ((xbits >> i) & 1u) ? -kCap : kCap, ((xbits >> (i + 1)) & 1u) ? -kCap : kCap,
+                                ((xbits >> (i + 2)) & 1u) ? -kCap : kCap, ((xbits >> (i + 3)) & 1u) ? -kCap : kCap);
+                    } else {
+#pragma unroll 1
+                        for (int i = 0; i < W; ++i) {
+                            const int j = j0 + i;
+                            reinterpret_cast<float*>(&base[(j >> 2) * 32 + lane])[j & 3] =
+                                ((xbits >> i) & 1u) ? -kCap : kCap;
+                        }
+                    }
                 }
+                if (T != M) {
+                    const int ps = PL::NLR + __popc(SMEMM & ((1u << T) - 1u));
+                    sm->pm[ps][lane] |= msk;
+                    if (__any_sync(kFull, msk != 0u)) prot |= 1u << ps;
+                }
+            } else if ((REGM >> T) & 1u) {
+                const int sl = __popc(REGM & ((1u << T) - 1u));
+                sm->pm[sl][lane] |= msk;
+                sm->ss[sl][lane] = (sm->ss[sl][lane] & ~msk) | ((xbits << j0) & msk);
+                if (__any_sync(kFull, msk != 0u)) prot |= 1u << sl;
+            } else {  // pass boundary: re-saturated before its next read
+                if (lane == 0) sm->xprot[T / K - 1][bi >> 5] |= 1u << (bi & 31);
+                scatter(sm->sat, xbits, in_block, b, q, W, j0, start);
             }
-            const int ps = PL::NLR + __popc(SMEMM & ((1u << T) - 1u));
-            sm->pm[ps][lane] |= msk;
-            if (__any_sync(kFull, msk != 0u)) prot |= 1u << ps;
-        } else if ((REGM >> T) & 1u) {
-            const int sl = __popc(REGM & ((1u << T) - 1u));
-            sm->pm[sl][lane] |= msk;
-            sm->ss[sl][lane] = (sm->ss[sl][lane] & ~msk) | ((xbits << j0) & msk);
-            if (__any_sync(kFull, msk != 0u)) prot |= 1u << sl;
-        } else {  // pass boundary: re-saturated before its next read
-            if (lane == 0) sm->xprot[T / K - 1][bi >> 5] |= 1u << (bi & 31);
-            scatter(sm->sat, xbits, in_block, b, q, W, j0, start);
+            // 2. decided_u (csfg_freeze.cpp:87)
+            scatter(sm->dec_u, ubits, in_block, b, q, W, j0, start);
+            // 3. inactive top rows of the stages after S. Only the first commit of
+            //    an iteration can re-cover rows decided before (later blocks start
+            //    at the frontier), so freeze_stage still holds their old stages.
+            if (k == 0 && start < fr_start) {
+                sm->tmp[lane] = 0;
+                __syncwarp();
+#pragma unroll 1
+                for (int r = start + lane; r < fr_start; r += 32) {
+                    const int fo = sm->fst[r];
+#pragma unroll 1
+                    for (int s2 = S + 1; s2 < M; ++s2)
+                        if (fo < s2 && !((r >> (M - 1 - s2)) & 1)) atomicAdd(&sm->tmp[s2], 1);
+                }
+                __syncwarp();
+                if (lane > S && lane < M) dinact += (sz >> 1) - sm->tmp[lane];
+                __syncwarp();
+            } else if (lane > S && lane < M) {
+                dinact += sz >> 1;
+            }
+            //    freeze_stage over the block (csfg_freeze.cpp:86)
+            if (sz >= 4) {
+                const uint32_t w4 = 0x01010101u * (uint32_t)S;
+#pragma unroll 1
+                for (int i = 4 * lane; i < sz; i += 128) *reinterpret_cast<uint32_t*>(&sm->fst[start + i]) = w4;
+            } else if (lane < sz) {
+                sm->fst[start + lane] = (uint8_t)S;
+            }
+            // 4. event log (csfg_freeze.cpp:91-92)
+            if (lane == 0 && a->events && nev < a->ev_cap) {
+                int* e = a->events + ((long long)frame_ * a->ev_cap + nev) * 5;
+                e[0] = it;
+                e[1] = S;
+                e[2] = bi;
+                e[3] = start;
+                e[4] = sz;
+            }
+            ++nev;
         }
-        scatter(sm->dec_u, ubits, in_block, b, q, W, j0, start);
-        commit_counts(S, start, sz, frontier);
-        if (lane == 0 && a->events && nev < a->ev_cap) {
-            int* e = a->events + ((long long)frame_ * a->ev_cap + nev) * 5;
-            e[0] = it;
-            e[1] = S;
-            e[2] = bi;
-            e[3] = start;
-            e[4] = sz;
-        }
-        ++nev;
-        frontier = start + sz;
+        if (lane < M) sm->inact[lane] += dinact;
         __syncwarp();
-    }
-
-    // inact[S+1 ..] and freeze_stage over the block [start, start+sz); rows of
-    // [start, fr0) were decided earlier (an enclosing block supersedes them).
-    // Returns the increase of sum(inact).
-    __device__ __forceinline__ int commit_counts(int S, int start, int sz, int fr0) {  // returns added inactive rows
-        int add;
-        if (start < fr0) {
-            sm->tmp[lane] = 0;
-            __syncwarp();
-#pragma unroll 1
-            for (int r = start + lane; r < fr0; r += 32) {
-                const int fo = sm->fst[r];
-#pragma unroll 1
-                for (int s2 = S + 1; s2 < M; ++s2)
-                    if (fo < s2 && !((r >> (M - 1 - s2)) & 1)) atomicAdd(&sm->tmp[s2], 1);
-            }
-            __syncwarp();
-            int v = 0;
-            if (lane > S && lane < M) {
-                v = (sz >> 1) - sm->tmp[lane];
-                sm->inact[lane] += v;
-            }
-            add = __reduce_add_sync(kFull, v);
-        } else {
-            if (lane > S && lane < M) sm->inact[lane] += (sz >> 1);
-            add = (M - 1 - S) * (sz >> 1);
-        }
-#pragma unroll 1
-        for (int i = lane; i < sz; i += 32) sm->fst[start + i] = (uint8_t)S;
-        __syncwarp();
-        return add;
     }
 
     // write W block bits of a pass layout (base bit b) into row-order words
@@ -629,7 +681,9 @@ struct Dec {
         store_L<S>(Lt);
         if constexpr (last_of_pass && S + 1 < M) x_store<q>(sm->X[q], R);
         if constexpr (first_of_pass || (last_of_pass && S + 1 < M)) __syncwarp();
+#ifndef PBP_DBG_NOSNAP
         if constexpr (KIND == 2) snapshot<S>();
+#endif
         return true;
     }
 
@@ -847,8 +901,11 @@ struct Dec {
 #pragma unroll 1
             for (int i = lane; i < PL::NX; i += 32) sm->X[x][i] = 0.f;
         // L(m): +CAP at frozen rows (bp_core.cpp:53), last-pass layout
-        sm->lmz[lane] = FZ[Q - 1];
-        sm->lms[lane] = 0u;
+        const uint32_t fl = FZ[Q - 1];
+#pragma unroll 1
+        for (int c = 0; c < P / 4; ++c)
+            sm->LM[c][lane] = make_float4(((fl >> (4 * c)) & 1u) ? kCap : 0.f, ((fl >> (4 * c + 1)) & 1u) ? kCap : 0.f,
+                                          ((fl >> (4 * c + 2)) & 1u) ? kCap : 0.f, ((fl >> (4 * c + 3)) & 1u) ? kCap : 0.f);
         if (lane < NW) sm->dec_u[lane] = 0u;
 #pragma unroll 1
         for (int x = 0; x < Q - 1; ++x)
