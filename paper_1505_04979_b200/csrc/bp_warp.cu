@@ -36,6 +36,8 @@
 // (read-side override for register arrays, predicated stores for shared
 // slots, re-saturation for X). PE activations are counted by the reference
 // rule from per-stage inactive-row counts.
+#include <type_traits>
+
 #include "pbp_common.cuh"
 
 namespace pbp {
@@ -91,6 +93,10 @@ struct Plan {
     static constexpr int NLS = n_smem() > 0 ? n_smem() : 1;
     // protection-mask slot of array L(s): register arrays first, then shared ones
     static constexpr int prot_slot(int s) { return local_reg(s) ? reg_slot(s) : NLR + smem_slot(s); }
+    // csfg: stages of the last pass (base bit 0) keep every candidate block
+    // inside one lane; those checks read raw R rows of two lanes (see snap_rows)
+    static constexpr int SL = (Q - 1) * K;  // first stage of the last pass
+    static constexpr int NL = M - SL;       // stages in the last pass
 };
 
 template <int M>
@@ -108,9 +114,12 @@ struct WarpSmem {
     int inact[32];                         // inactive top rows per stage
     int tmp[32];
     unsigned long long cnt[16];            // per-warp counter accumulators
-    uint32_t su[PL::M][32];                // per stage: block-transformed sign bits of R(s+1)
-    uint32_t sv[PL::M][32];                // per stage: violated groups, OR over a block's lanes
-    int cS[PL::M], cbi[PL::M];             // commits recorded by the walk of one iteration
+    uint32_t su[PL::SL][32];               // per stage < SL: block-transformed sign bits of R(s+1)
+    uint32_t sv[PL::SL][32];               // ... and violated groups, OR over a block's lanes
+    float rs[PL::NL][2][PL::P];            // per stage >= SL: R(s+1) of the two candidate lanes
+    int cS[PL::M], cbi[PL::M];             // commits recorded by the walks of one iteration
+    uint32_t cX[PL::M], cU[PL::M];         // last-pass commits: x_hat / u_hat of the block (row order)
+    uint32_t frz[PL::NW];                  // frozen rows, row-order words
     uint32_t fz[PL::Q][32];                // frozen rows per pass layout
     uint8_t fst[PL::N];                    // freeze_stage per row
 };
@@ -154,8 +163,29 @@ __device__ __forceinline__ uint32_t jmask(int tp) {
          : tp == 3 ? 0x00FF00FFu : 0x0000FFFFu;
 }
 
+#ifdef PBP_PROF_SECTIONS
+// timing experiments only: per-warp clock64 time per code section
+__device__ unsigned long long g_prof[8];
+extern "C" int pbp_prof_read(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, g_prof, sizeof(g_prof)) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+    }
+    return 0;
+}
+#define PBP_T0(v) const long long v = clock64()
+#define PBP_T1(v, k) do { if (lane == 0) prof[k] += clock64() - (v); } while (0)
+#else
+#define PBP_T0(v)
+#define PBP_T1(v, k)
+#endif
+
 template <int M, int KIND>
 struct Dec {
+#ifdef PBP_PROF_SECTIONS
+    unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
     using PL = Plan<M>;
     static constexpr int N = PL::N, P = PL::P, K = PL::K, Q = PL::Q, NW = PL::NW;
 
@@ -169,6 +199,11 @@ struct Dec {
     uint32_t FZ[Q];  // frozen rows per pass layout (bit j = row_of<q>(j))
 
     int frontier, nev, it;
+    // csfg walk state of the current iteration
+    int L1;        // lane of the frontier when the last pass starts (candidate rows: L1, L1+1)
+    int nc_, nce_; // commits recorded / of them by the early walk (stages < SL)
+    int s_last_, fr_start_;
+    bool done_;    // the frontier reached n
     uint32_t prot;   // bit per protection slot: some lane holds a frozen-boundary row
     long long act, frame_;
     uint32_t xq;     // channel-side decisions of stage 0, permuted pass-0 layout
@@ -423,56 +458,79 @@ struct Dec {
         return m;
     }
 
-    // Sweep side of the check for stage S: x_hat = sign bits of R(S+1) and its
-    // polar transform inside every block-sized register group of every lane
-    // (all candidate positions at once, straight-line code), then the frozen-row
-    // violations OR-ed over the lanes a block spans (its lane_lo bits): sv[S][l]
-    // tells, for the lane group of l, which register groups would be rejected.
+    // Sweep side of the check for stage S < SL: the sign bits of R(S+1) of
+    // this lane's rows (bit j = row_of(j)); the rest happens in verdicts().
     template <int S>
     __device__ __forceinline__ void snapshot() {
+        sm->su[S][lane] = pack_all();
+    }
+
+    // For every stage S < SL: x_hat's polar transform inside every block (all
+    // candidate positions at once): in-word for the register bits, shfl_xor
+    // for the lane bits; then the frozen-row violations OR-ed over the lanes a
+    // block spans (its lane_lo bits). sv[S][l] tells, for the lane group of l,
+    // which register groups would be rejected; su[S] keeps u_hat. Run once per
+    // iteration off the sweep's straight line, the stages' independent
+    // shuffle chains interleaved.
+    template <int S>
+    __device__ __forceinline__ void verdict_of(uint32_t& u, uint32_t& v) {
         constexpr int q = PL::pass_of(S);
         constexpr int b = PL::base_bit(q);
-        constexpr int g = M - 1 - S;
-        uint32_t u = pack_all();
+        constexpr int g = M - 1 - S;  // >= b before the last pass
 #pragma unroll
         for (int tp = 0; tp < g - b; ++tp) u ^= (u >> (1 << tp)) & jmask(tp);
 #pragma unroll
-        for (int gp = 0; gp < (g < b ? g : b); ++gp) {
+        for (int gp = 0; gp < b; ++gp) {
             const uint32_t o = __shfl_xor_sync(kFull, u, 1 << gp);
             if (!((lane >> gp) & 1)) u ^= o;
         }
-        uint32_t v = u & FZ[q];
+        v = u & FZ[q];
         if constexpr (b == 5) {
             v = __reduce_or_sync(kFull, v);
         } else {
 #pragma unroll
             for (int gp = 0; gp < b; ++gp) v |= __shfl_xor_sync(kFull, v, 1 << gp);
         }
-        sm->sv[S][lane] = v;
-        sm->su[S][lane] = u;
+    }
+    template <int S>
+    __device__ __forceinline__ void verdicts_from(uint32_t (&u)[PL::SL], uint32_t (&v)[PL::SL]) {
+        verdict_of<S>(u[S], v[S]);
+        if constexpr (S + 1 < PL::SL) verdicts_from<S + 1>(u, v);
+    }
+    __device__ __forceinline__ void verdicts() {
+        uint32_t u[PL::SL], v[PL::SL];
+#pragma unroll
+        for (int S = 0; S < PL::SL; ++S) u[S] = sm->su[S][lane];
+        verdicts_from<0>(u, v);
+#pragma unroll
+        for (int S = 0; S < PL::SL; ++S) {
+            sm->sv[S][lane] = v[S];
+            sm->su[S][lane] = u[S];
+        }
     }
 
-    // The reference's stage loop (csfg_freeze.cpp:109-119) replayed after the
-    // sweep, in two phases. (1) Walk: between two commits the frontier is
-    // fixed, so lane s evaluates stage s's candidate for the current frontier
-    // and one ballot finds the first accepting stage; stages before it reject,
-    // it commits, the frontier moves, the rest are evaluated again. Only the
-    // frontier is needed for that. (2) The side effects of the recorded commits
-    // (apply_freeze) in order, with one trailing __syncwarp. Returns
-    // frontier < n (the reference then runs the pinned G-check).
-    __device__ __forceinline__ bool chain() {
-#ifdef PBP_DBG_NOCHAIN  // timing experiments only: results are wrong
-        act += (long long)M * (N >> 1);
-        return frontier < N;
-#endif
-        __syncwarp();  // snapshots of the whole warp
-        int s_next = 0, s_last = M - 1, nc = 0;
-        const int fr_start = frontier;
-        bool done = false;
+    // The reference's stage loop (csfg_freeze.cpp:109-119), replayed in two
+    // walks. Between two commits the frontier is fixed, so lane s evaluates
+    // stage s's candidate for the current frontier and one ballot finds the
+    // first accepting stage; stages before it reject, it commits, the frontier
+    // moves, the rest are evaluated again. The early walk (stages < SL, from
+    // the snapshots' verdicts) runs when the sweep reaches the last pass; it
+    // fixes the lane whose rows can still hold candidates (L1, L1+1), whose
+    // R(s+1) the last pass then stores raw. The late walk checks the last-pass
+    // stages on those rows. Side effects (apply_freeze) follow after the sweep.
+    __device__ __forceinline__ void walk_early() {
+        verdicts();
+        __syncwarp();  // verdicts of the whole warp
+        constexpr int SL = PL::SL;
+        fr_start_ = frontier;
+        nc_ = 0;
+        s_last_ = M - 1;
+        done_ = false;
+        int s_next = 0;
 #pragma unroll 1
-        while (s_next < M) {
+        while (s_next < SL) {
             bool acc = false;
-            if (lane >= s_next && lane < M) {
+            if (lane >= s_next && lane < SL) {
                 const int st = lane;
                 const int q = st / K;
                 const int b = (M - K - q * K) > 0 ? (M - K - q * K) : 0;
@@ -489,35 +547,125 @@ struct Dec {
             const int st = __ffs(am) - 1;
             const int g = M - 1 - st;
             if (lane == 0) {
-                sm->cS[nc] = st;
-                sm->cbi[nc] = frontier >> g;
+                sm->cS[nc_] = st;
+                sm->cbi[nc_] = frontier >> g;
             }
-            ++nc;
+            ++nc_;
             frontier = ((frontier >> g) + 1) << g;
             if (frontier >= N) {
-                s_last = st;
-                done = true;
+                s_last_ = st;
+                done_ = true;
                 break;
             }
             s_next = st + 1;
         }
-        if (nc) apply_commits(nc, fr_start);
-        // stage_pass counts of stages 0..s_last under the freeze state each ran
-        // with (a commit at stage s only changes inact[s' > s])
-        const int v = lane <= s_last ? (N >> 1) - sm->inact[lane] : 0;
-        act += __reduce_add_sync(kFull, v);
-        return !done;
+        nce_ = nc_;
+        L1 = done_ ? -4 : frontier / P;
     }
 
-    // apply_freeze (csfg_freeze.cpp:82-93) for the commits of one iteration,
-    // in order: saturate/protect L(S+1), decided_u, inactive-PE counts,
-    // freeze_stage, event log.
-    __device__ __forceinline__ void apply_commits(int nc, int fr_start) {
+    // last-pass stage S: lanes L1 and L1+1 keep R(S+1) (rows P*lane + j)
+    template <int S>
+    __device__ __forceinline__ void snap_rows() {
+        const unsigned c = (unsigned)(lane - L1);
+        if (c < 2u) {
+            float4* d = reinterpret_cast<float4*>(&sm->rs[S - PL::SL][c][0]);
+#pragma unroll
+            for (int i = 0; i < P / 4; ++i) d[i] = make_float4(R[4 * i], R[4 * i + 1], R[4 * i + 2], R[4 * i + 3]);
+        }
+    }
+
+    __device__ __forceinline__ void walk_late() {
+        constexpr int SL = PL::SL, NL = PL::NL;
+        __syncwarp();  // rs rows
+        if (done_) return;
+        // sign bits of rows P*L1 + i (i < 2P) after each last-pass stage; lane t
+        // keeps stage SL + t's
+        using WT = typename std::conditional<(P == 32), unsigned long long, uint32_t>::type;
+        WT wv = 0;
+#pragma unroll
+        for (int t = 0; t < NL; ++t) {
+            WT w;
+            if constexpr (P == 32) {
+                const uint32_t lo = __ballot_sync(kFull, __float_as_int(sm->rs[t][0][lane]) < 0);
+                const uint32_t hi = __ballot_sync(kFull, __float_as_int(sm->rs[t][1][lane]) < 0);
+                w = (WT)lo | ((WT)hi << 32);
+            } else {
+                const float* f = &sm->rs[t][0][0];
+                const float v = lane < 2 * P ? f[lane] : 0.f;
+                w = __ballot_sync(kFull, lane < 2 * P && __float_as_int(v) < 0);
+            }
+            if (lane == t) wv = w;
+        }
+        const int row0 = P * L1;
+        int s_next = SL;
+#pragma unroll 1
+        for (;;) {
+            bool acc = false;
+            uint32_t xb = 0u, ub = 0u;
+            const int st = SL + lane;
+            if (lane < NL && st >= s_next) {
+                const int g = M - 1 - st;
+                const int A = (frontier >> g) << g;
+                const uint32_t wm = (1u << (1 << g)) - 1u;  // block of 2^g <= 16 rows
+                xb = (uint32_t)(wv >> (A - row0)) & wm;
+                ub = xb;
+#pragma unroll
+                for (int tp = 0; tp < K - 1; ++tp)
+                    if (tp < g) ub ^= (ub >> (1 << tp)) & jmask(tp);
+                const uint32_t fzb = (sm->frz[A >> 5] >> (A & 31)) & wm;
+                acc = (ub & fzb) == 0u;
+            }
+            const uint32_t am = __ballot_sync(kFull, acc);
+            if (!am) break;
+            const int t = __ffs(am) - 1;
+            const int st2 = SL + t;
+            const int g = M - 1 - st2;
+            if (lane == t) {
+                sm->cS[nc_] = st2;
+                sm->cbi[nc_] = frontier >> g;
+                sm->cX[nc_] = xb;
+                sm->cU[nc_] = ub;
+            }
+            ++nc_;
+            frontier = ((frontier >> g) + 1) << g;
+            if (frontier >= N) {
+                s_last_ = st2;
+                done_ = true;
+                break;
+            }
+            s_next = st2 + 1;
+            if (s_next >= M) break;
+        }
+    }
+
+    // after the sweep: late walk, side effects, stage_pass counts of stages
+    // 0..s_last under the freeze state each ran with (a commit at stage s only
+    // changes inact[s' > s]). Returns frontier < n (the reference then runs the
+    // pinned G-check).
+    __device__ __forceinline__ bool finish_iter() {
+        PBP_T0(tw);
+        walk_late();
+        PBP_T1(tw, 3);
+        PBP_T0(ta);
+        if (nc_) apply_commits();
+        PBP_T1(ta, 4);
+        const int v = lane <= s_last_ ? (N >> 1) - sm->inact[lane] : 0;
+        act += __reduce_add_sync(kFull, v);
+        return !done_;
+    }
+
+    // apply_freeze (csfg_freeze.cpp:82-93) for the commits of one iteration:
+    // saturate/protect L(S+1), decided_u, inactive-PE counts, freeze_stage,
+    // event log. Commits of the early walk one after the other with the whole
+    // warp (their blocks span lanes); last-pass commits one per lane (blocks
+    // are disjoint, their L(S+1) are different arrays).
+    __device__ __forceinline__ void apply_commits() {
         constexpr uint32_t REGM = mask_of(0), SMEMM = mask_of(1);
+        const int nc = nc_, nce = nce_, fr_start = fr_start_;
         __syncwarp();
         int dinact = 0;  // this lane's stage: newly inactive top rows
 #pragma unroll 1
-        for (int k = 0; k < nc; ++k) {
+        for (int k = 0; k < nce; ++k) {
             const int S = sm->cS[k], bi = sm->cbi[k];
             const int q = S / K;
             const int b = (M - K - q * K) > 0 ? (M - K - q * K) : 0;
@@ -614,8 +762,104 @@ struct Dec {
             }
             ++nev;
         }
+        if (nc > nce) apply_last(nce, nc, fr_start, dinact);
         if (lane < M) sm->inact[lane] += dinact;
         __syncwarp();
+    }
+
+    // last-pass commits k in [k0, nc): lane k applies commit k
+    __device__ __forceinline__ void apply_last(int k0, int nc, int fr_start, int& dinact) {
+        constexpr uint32_t REGM = mask_of(0), SMEMM = mask_of(1);
+        const bool mine = lane >= k0 && lane < nc;
+        const int S = mine ? sm->cS[lane] : 0;
+        // inactive top rows: a stage-S block of sz rows has sz/2 top rows at
+        // every later stage (stages are distinct and increasing in one walk)
+        const uint32_t cm = __reduce_or_sync(kFull, mine ? (1u << S) : 0u);
+        if (lane < M) dinact += (int)((__brev(cm & ((1u << lane) - 1u)) >> (32 - M)) >> 1);
+        if (k0 == 0) {
+            // the first commit of the iteration may re-cover decided rows
+            // [A, fr_start) (< 32 of them): those already inactive at a stage
+            // s2 > S0 under their old freeze_stage are not counted twice
+            const int S0 = sm->cS[0], g0 = M - 1 - S0;
+            const int A0 = sm->cbi[0] << g0;
+            if (A0 < fr_start) {
+                const int r = A0 + lane;
+                uint32_t was = 0u;
+                if (r < fr_start) {
+                    const int fo = sm->fst[r];
+#pragma unroll
+                    for (int s2 = 1; s2 < M; ++s2)
+                        if (s2 > S0 && fo < s2 && !((r >> (M - 1 - s2)) & 1)) was |= 1u << s2;
+                }
+#pragma unroll
+                for (int s2 = 1; s2 < M; ++s2) {
+                    const int c = __popc(__ballot_sync(kFull, (was >> s2) & 1u));
+                    if (lane == s2) dinact -= c;
+                }
+            }
+            __syncwarp();  // freeze_stage reads before the writes below
+        }
+        uint32_t myprot = 0u;
+        if (mine) {
+            const int g = M - 1 - S, W = 1 << g;
+            const int A = sm->cbi[lane] << g;
+            const uint32_t xb = sm->cX[lane], ub = sm->cU[lane];
+            const uint32_t wm = (1u << W) - 1u;
+            const int owner = A / P, j0 = A % P;  // last-pass layout: row = P*lane + j
+            const int T = S + 1;
+            // 1. saturate / protect L(S+1) (csfg_freeze.cpp:84-86)
+            if (T == M || ((SMEMM >> T) & 1u)) {
+                float* base = (T == M) ? reinterpret_cast<float*>(&sm->LM[0][0])
+                                       : reinterpret_cast<float*>(&sm->Ls[__popc(SMEMM & ((1u << T) - 1u))][0][0]);
+                if (W >= 4) {
+#pragma unroll 1
+                    for (int i = 0; i < W; i += 4)
+                        reinterpret_cast<float4*>(base)[((j0 + i) >> 2) * 32 + owner] = make_float4(
+                            ((xb >> i) & 1u) ? -kCap : kCap, ((xb >> (i + 1)) & 1u) ? -kCap : kCap,
+                            ((xb >> (i + 2)) & 1u) ? -kCap : kCap, ((xb >> (i + 3)) & 1u) ? -kCap : kCap);
+                } else {
+#pragma unroll 1
+                    for (int i = 0; i < W; ++i) {
+                        const int j = j0 + i;
+                        base[((j >> 2) * 32 + owner) * 4 + (j & 3)] = ((xb >> i) & 1u) ? -kCap : kCap;
+                    }
+                }
+                if (T != M) {
+                    const int ps = PL::NLR + __popc(SMEMM & ((1u << T) - 1u));
+                    sm->pm[ps][owner] |= wm << j0;
+                    myprot = 1u << ps;
+                }
+            } else {  // register array in the last-pass layout
+                const int sl = __popc(REGM & ((1u << T) - 1u));
+                sm->pm[sl][owner] |= wm << j0;
+                sm->ss[sl][owner] = (sm->ss[sl][owner] & ~(wm << j0)) | (xb << j0);
+                myprot = 1u << sl;
+            }
+            // 2. decided_u (csfg_freeze.cpp:87)
+            atomicAnd(&sm->dec_u[A >> 5], ~(wm << (A & 31)));
+            atomicOr(&sm->dec_u[A >> 5], ub << (A & 31));
+            // 3. freeze_stage over the block (csfg_freeze.cpp:86)
+            if (W >= 4) {
+                const uint32_t w4 = 0x01010101u * (uint32_t)S;
+#pragma unroll 1
+                for (int i = 0; i < W; i += 4) *reinterpret_cast<uint32_t*>(&sm->fst[A + i]) = w4;
+            } else {
+                sm->fst[A] = (uint8_t)S;
+                if (W == 2) sm->fst[A + 1] = (uint8_t)S;
+            }
+            // 4. event log (csfg_freeze.cpp:91-92)
+            const int e_ix = nev + (lane - k0);
+            if (a->events && e_ix < a->ev_cap) {
+                int* e = a->events + ((long long)frame_ * a->ev_cap + e_ix) * 5;
+                e[0] = it;
+                e[1] = S;
+                e[2] = A >> g;
+                e[3] = A;
+                e[4] = W;
+            }
+        }
+        prot |= __reduce_or_sync(kFull, myprot);
+        nev += nc - k0;
     }
 
     // write W block bits of a pass layout (base bit b) into row-order words
@@ -670,20 +914,31 @@ struct Dec {
             x_load<q>(sm->X[q - 1], R);
         }
         if constexpr (PL::is_boundary(S + 1)) {
+            PBP_T0(tr);
             if constexpr (KIND == 2)
                 resaturate<PL::pass_of(S + 1)>();
             else
                 __syncwarp();  // X holds other lanes' L(e) writes of the previous iteration
+            PBP_T1(tr, 2);
         }
+        PBP_T0(tm);
         float Lt[P];
         load_L<S + 1>(Lt);
         pe_stage<S>(Lt);
         store_L<S>(Lt);
         if constexpr (last_of_pass && S + 1 < M) x_store<q>(sm->X[q], R);
         if constexpr (first_of_pass || (last_of_pass && S + 1 < M)) __syncwarp();
-#ifndef PBP_DBG_NOSNAP
-        if constexpr (KIND == 2) snapshot<S>();
-#endif
+        PBP_T1(tm, 0);
+        if constexpr (KIND == 2) {
+            PBP_T0(ts);
+            if constexpr (S < PL::SL) {
+                snapshot<S>();
+                if constexpr (S == PL::SL - 1) walk_early();
+            } else {
+                snap_rows<S>();
+            }
+            PBP_T1(ts, 1);
+        }
         return true;
     }
 
@@ -743,6 +998,7 @@ struct Dec {
         lane = ln;
         alpha = args.alpha;
         fz_init<0>();
+        if (lane < NW) sm->frz[lane] = a->frozen_bits[lane];
         // stage 0 pushes x_hat bits of rows (lane + 32 j) in the order
         // j = j0, j0+1, j0+d, j0+d+1 for j0 = 0, 2, ... (d = P/2); the first push
         // lands in bit 31. xperm = bit position that holds row-order word `lane`.
@@ -763,6 +1019,7 @@ struct Dec {
             f = __shfl_sync(kFull, f, 0);
             if (f >= args.frames) break;
             frame_ = f;
+            PBP_T0(tf);
             if (!load_frame(f)) {
                 if (lane == 0) {
                     const unsigned long long slot = atomicAdd(args.list_len, 1ull);
@@ -771,6 +1028,8 @@ struct Dec {
                 continue;
             }
             init_frame();
+            PBP_T1(tf, 6);
+            PBP_T0(tl);
             int iters = (KIND == 0) ? args.max_iter : 0;
             int stop = 0;
             bool converged = false;
@@ -783,7 +1042,11 @@ struct Dec {
                 it = t;
                 sweep_from<0>();
                 if constexpr (KIND == 2) {
-                    if (chain()) converged = gcheck(frontier);
+                    if (finish_iter()) {
+                        PBP_T0(tg);
+                        converged = gcheck(frontier);
+                        PBP_T1(tg, 5);
+                    }
                 } else {
                     act += (long long)M * (N >> 1);
                 }
@@ -795,6 +1058,7 @@ struct Dec {
                     }
                 }
             }
+            PBP_T1(tl, 7);
             if constexpr (KIND == 1) {
                 if (stop == 0) iters = args.max_iter;
             }
@@ -812,6 +1076,10 @@ struct Dec {
         }
         if (args.counters && lane < kNumCounters && sm->cnt[lane])
             atomicAdd(&args.counters[lane], sm->cnt[lane]);
+#ifdef PBP_PROF_SECTIONS
+        if (lane == 0)
+            for (int i = 0; i < 8; ++i) atomicAdd(&g_prof[i], prof[i]);
+#endif
     }
 
     __device__ __forceinline__ void write_outputs(long long f, uint32_t uw, int iters, int stop) {

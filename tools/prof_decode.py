@@ -35,3 +35,19 @@ for r in range(a.reps):
     c = cnt.cpu().tolist()
     print(f"rep {r}: {dt*1e3:.2f} ms  {a.frames/dt/1e6:.3f} Mframes/s  avg iters {c[3]/c[0]:.2f}  "
           f"PE/s {c[5]/dt:.3e}  ({c[5]*9/dt/1e12:.2f} TOP/s)")
+if hasattr(P.lib, "pbp_prof_read") and os.environ.get("PBP_LIB"):
+    # library built with -DPBP_PROF_SECTIONS: per-warp clock64 split of the last rep
+    buf = (C.c_ulonglong * 8)()
+    P.lib.pbp_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+    P.lib.pbp_prof_read(buf, 1)
+    cnt.zero_()
+    P._check(P.lib.pbp_decode_count_device(ctx.handle, C.byref(cs), kind, P._abi.f32p(llr.data_ptr()),
+                                           P._abi.u32p(u.data_ptr()), a.frames, 0.9375, 40,
+                                           P._abi.i64p(cnt.data_ptr()), None))
+    ctx.synchronize()
+    P.lib.pbp_prof_read(buf, 1)
+    names = ["stage math", "snapshot", "resat/sync", "walk", "commits", "gcheck", "frame load", "iter loop"]
+    tot = buf[7] + buf[6]
+    its = cnt.cpu().tolist()[3]
+    for i, nm in enumerate(names):
+        print(f"  {nm:12s} {buf[i]/tot*100:6.1f}%  {buf[i]/its:9.1f} clk/iter")
