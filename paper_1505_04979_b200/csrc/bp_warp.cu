@@ -111,14 +111,12 @@ struct WarpSmem {
     uint32_t dec_u[PL::NW];                // decided_u bits (row order)
     uint32_t sat[PL::NW];                  // x_hat of the latest commit per row
     uint32_t xprot[PL::Q - 1][PL::NW];     // per boundary: blocks frozen at stage e-1
-    int inact[32];                         // inactive top rows per stage
     int tmp[32];
     unsigned long long cnt[16];            // per-warp counter accumulators
     uint32_t su[PL::SL][32];               // per stage < SL: block-transformed sign bits of R(s+1)
     uint32_t sv[PL::SL][32];               // ... and violated groups, OR over a block's lanes
     float rs[PL::NL][2][PL::P];            // per stage >= SL: R(s+1) of the two candidate lanes
     int cS[PL::M], cbi[PL::M];             // commits recorded by the walks of one iteration
-    uint32_t cX[PL::M], cU[PL::M];         // last-pass commits: x_hat / u_hat of the block (row order)
     uint32_t frz[PL::NW];                  // frozen rows, row-order words
     uint32_t fz[PL::Q][32];                // frozen rows per pass layout
     uint8_t fst[PL::N];                    // freeze_stage per row
@@ -199,9 +197,10 @@ struct Dec {
     uint32_t FZ[Q];  // frozen rows per pass layout (bit j = row_of<q>(j))
 
     int frontier, nev, it;
+    int inact;     // lane s < M: inactive top rows of stage s
     // csfg walk state of the current iteration
     int L1;        // lane of the frontier when the last pass starts (candidate rows: L1, L1+1)
-    int nc_, nce_; // commits recorded / of them by the early walk (stages < SL)
+    int nce_;      // commits of the early walk (stages < SL)
     int s_last_, fr_start_;
     bool done_;    // the frontier reached n
     uint32_t prot;   // bit per protection slot: some lane holds a frozen-boundary row
@@ -523,7 +522,7 @@ struct Dec {
         __syncwarp();  // verdicts of the whole warp
         constexpr int SL = PL::SL;
         fr_start_ = frontier;
-        nc_ = 0;
+        int nc = 0;
         s_last_ = M - 1;
         done_ = false;
         int s_next = 0;
@@ -547,10 +546,10 @@ struct Dec {
             const int st = __ffs(am) - 1;
             const int g = M - 1 - st;
             if (lane == 0) {
-                sm->cS[nc_] = st;
-                sm->cbi[nc_] = frontier >> g;
+                sm->cS[nc] = st;
+                sm->cbi[nc] = frontier >> g;
             }
-            ++nc_;
+            ++nc;
             frontier = ((frontier >> g) + 1) << g;
             if (frontier >= N) {
                 s_last_ = st;
@@ -559,7 +558,7 @@ struct Dec {
             }
             s_next = st + 1;
         }
-        nce_ = nc_;
+        nce_ = nc;
         L1 = done_ ? -4 : frontier / P;
     }
 
@@ -574,13 +573,17 @@ struct Dec {
         }
     }
 
-    __device__ __forceinline__ void walk_late() {
+    // Late walk. Lane t < NL takes stage SL + t: the sign bits x of rows
+    // P*L1 + i (i < 2P) after that stage, their transform u inside each
+    // 2^g-row block, and a bitmap of rejected blocks (bit at each block's first
+    // row), so a round of the walk is one bit test per lane. A committing lane
+    // keeps its block start in lA (a stage commits at most once per iteration).
+    using WT = typename std::conditional<(P == 32), unsigned long long, uint32_t>::type;
+    __device__ __forceinline__ void walk_late(WT& xw, WT& uw, int& lA, uint32_t& cmask) {
         constexpr int SL = PL::SL, NL = PL::NL;
         __syncwarp();  // rs rows
+        cmask = 0u;
         if (done_) return;
-        // sign bits of rows P*L1 + i (i < 2P) after each last-pass stage; lane t
-        // keeps stage SL + t's
-        using WT = typename std::conditional<(P == 32), unsigned long long, uint32_t>::type;
         WT wv = 0;
 #pragma unroll
         for (int t = 0; t < NL; ++t) {
@@ -597,43 +600,51 @@ struct Dec {
             if (lane == t) wv = w;
         }
         const int row0 = P * L1;
+        const int g = M - 1 - (SL + lane);  // this lane's stage (lane < NL)
+        xw = wv;
+        uw = wv;
+        WT viol;
+        {
+            const int w0 = row0 >> 5;
+            if constexpr (P == 32) {
+                viol = (WT)sm->frz[w0] | ((WT)(w0 + 1 < NW ? sm->frz[w0 + 1] : 0u) << 32);
+            } else {
+                const unsigned long long f2 =
+                    (unsigned long long)sm->frz[w0] | ((unsigned long long)(w0 + 1 < NW ? sm->frz[w0 + 1] : 0u) << 32);
+                viol = (WT)(f2 >> (row0 & 31));
+            }
+        }
+#pragma unroll
+        for (int tp = 0; tp < K - 1; ++tp) {
+            const WT jm = (WT)jmask(tp) | ((WT)jmask(tp) << (sizeof(WT) * 8 - 32));
+            if (tp < g) uw ^= (uw >> (1 << tp)) & jm;
+        }
+        viol &= uw;
+#pragma unroll
+        for (int tp = 0; tp < K - 1; ++tp)
+            if (tp < g) viol |= viol >> (1 << tp);
         int s_next = SL;
 #pragma unroll 1
         for (;;) {
             bool acc = false;
-            uint32_t xb = 0u, ub = 0u;
-            const int st = SL + lane;
-            if (lane < NL && st >= s_next) {
-                const int g = M - 1 - st;
+            if (lane < NL && SL + lane >= s_next) {
                 const int A = (frontier >> g) << g;
-                const uint32_t wm = (1u << (1 << g)) - 1u;  // block of 2^g <= 16 rows
-                xb = (uint32_t)(wv >> (A - row0)) & wm;
-                ub = xb;
-#pragma unroll
-                for (int tp = 0; tp < K - 1; ++tp)
-                    if (tp < g) ub ^= (ub >> (1 << tp)) & jmask(tp);
-                const uint32_t fzb = (sm->frz[A >> 5] >> (A & 31)) & wm;
-                acc = (ub & fzb) == 0u;
+                acc = !((viol >> (A - row0)) & 1u);
             }
             const uint32_t am = __ballot_sync(kFull, acc);
             if (!am) break;
             const int t = __ffs(am) - 1;
-            const int st2 = SL + t;
-            const int g = M - 1 - st2;
-            if (lane == t) {
-                sm->cS[nc_] = st2;
-                sm->cbi[nc_] = frontier >> g;
-                sm->cX[nc_] = xb;
-                sm->cU[nc_] = ub;
-            }
-            ++nc_;
-            frontier = ((frontier >> g) + 1) << g;
+            const int gt = M - 1 - (SL + t);
+            const int A = (frontier >> gt) << gt;
+            if (lane == t) lA = A;
+            cmask |= 1u << t;
+            frontier = A + (1 << gt);
             if (frontier >= N) {
-                s_last_ = st2;
+                s_last_ = SL + t;
                 done_ = true;
                 break;
             }
-            s_next = st2 + 1;
+            s_next = SL + t + 1;
             if (s_next >= M) break;
         }
     }
@@ -644,12 +655,15 @@ struct Dec {
     // pinned G-check).
     __device__ __forceinline__ bool finish_iter() {
         PBP_T0(tw);
-        walk_late();
+        WT xw, uw;
+        int lA = 0;
+        uint32_t cmask;
+        walk_late(xw, uw, lA, cmask);
         PBP_T1(tw, 3);
         PBP_T0(ta);
-        if (nc_) apply_commits();
+        if (nce_ | cmask) apply_commits(xw, uw, lA, cmask);
         PBP_T1(ta, 4);
-        const int v = lane <= s_last_ ? (N >> 1) - sm->inact[lane] : 0;
+        const int v = lane <= s_last_ ? (N >> 1) - inact : 0;
         act += __reduce_add_sync(kFull, v);
         return !done_;
     }
@@ -659,9 +673,9 @@ struct Dec {
     // event log. Commits of the early walk one after the other with the whole
     // warp (their blocks span lanes); last-pass commits one per lane (blocks
     // are disjoint, their L(S+1) are different arrays).
-    __device__ __forceinline__ void apply_commits() {
+    __device__ __forceinline__ void apply_commits(WT xw, WT uw, int lA, uint32_t cmask) {
         constexpr uint32_t REGM = mask_of(0), SMEMM = mask_of(1);
-        const int nc = nc_, nce = nce_, fr_start = fr_start_;
+        const int nce = nce_, fr_start = fr_start_;
         __syncwarp();
         int dinact = 0;  // this lane's stage: newly inactive top rows
 #pragma unroll 1
@@ -762,26 +776,28 @@ struct Dec {
             }
             ++nev;
         }
-        if (nc > nce) apply_last(nce, nc, fr_start, dinact);
-        if (lane < M) sm->inact[lane] += dinact;
+        if (cmask) apply_last(xw, uw, lA, cmask, nce, fr_start, dinact);
+        if (lane < M) inact += dinact;
         __syncwarp();
     }
 
-    // last-pass commits k in [k0, nc): lane k applies commit k
-    __device__ __forceinline__ void apply_last(int k0, int nc, int fr_start, int& dinact) {
+    // last-pass commits: lane t applies its stage's (cmask bit t)
+    __device__ __forceinline__ void apply_last(WT xw, WT uw, int lA, uint32_t cmask, int nce, int fr_start,
+                                               int& dinact) {
         constexpr uint32_t REGM = mask_of(0), SMEMM = mask_of(1);
-        const bool mine = lane >= k0 && lane < nc;
-        const int S = mine ? sm->cS[lane] : 0;
+        constexpr int SL = PL::SL;
+        const bool mine = (cmask >> lane) & 1u;
         // inactive top rows: a stage-S block of sz rows has sz/2 top rows at
         // every later stage (stages are distinct and increasing in one walk)
-        const uint32_t cm = __reduce_or_sync(kFull, mine ? (1u << S) : 0u);
+        const uint32_t cm = cmask << SL;
         if (lane < M) dinact += (int)((__brev(cm & ((1u << lane) - 1u)) >> (32 - M)) >> 1);
-        if (k0 == 0) {
+        if (nce == 0) {
             // the first commit of the iteration may re-cover decided rows
             // [A, fr_start) (< 32 of them): those already inactive at a stage
             // s2 > S0 under their old freeze_stage are not counted twice
-            const int S0 = sm->cS[0], g0 = M - 1 - S0;
-            const int A0 = sm->cbi[0] << g0;
+            const int t0 = __ffs(cmask) - 1;
+            const int S0 = SL + t0;
+            const int A0 = __shfl_sync(kFull, lA, t0);
             if (A0 < fr_start) {
                 const int r = A0 + lane;
                 uint32_t was = 0u;
@@ -801,10 +817,12 @@ struct Dec {
         }
         uint32_t myprot = 0u;
         if (mine) {
+            const int S = SL + lane;
             const int g = M - 1 - S, W = 1 << g;
-            const int A = sm->cbi[lane] << g;
-            const uint32_t xb = sm->cX[lane], ub = sm->cU[lane];
+            const int A = lA;
             const uint32_t wm = (1u << W) - 1u;
+            const int off = A - P * L1;
+            const uint32_t xb = (uint32_t)(xw >> off) & wm, ub = (uint32_t)(uw >> off) & wm;
             const int owner = A / P, j0 = A % P;  // last-pass layout: row = P*lane + j
             const int T = S + 1;
             // 1. saturate / protect L(S+1) (csfg_freeze.cpp:84-86)
@@ -848,7 +866,7 @@ struct Dec {
                 if (W == 2) sm->fst[A + 1] = (uint8_t)S;
             }
             // 4. event log (csfg_freeze.cpp:91-92)
-            const int e_ix = nev + (lane - k0);
+            const int e_ix = nev + __popc(cmask & ((1u << lane) - 1u));
             if (a->events && e_ix < a->ev_cap) {
                 int* e = a->events + ((long long)frame_ * a->ev_cap + e_ix) * 5;
                 e[0] = it;
@@ -859,7 +877,7 @@ struct Dec {
             }
         }
         prot |= __reduce_or_sync(kFull, myprot);
-        nev += nc - k0;
+        nev += __popc(cmask);
     }
 
     // write W block bits of a pass layout (base bit b) into row-order words
@@ -1153,6 +1171,7 @@ struct Dec {
             for (int j = 0; j < P; ++j) Lr[sl][j] = 0.f;
         init_smem();
         frontier = 0;
+        inact = 0;
         nev = 0;
         act = 0;
         prot = 0u;
@@ -1180,7 +1199,6 @@ struct Dec {
             if (lane < NW) sm->xprot[x][lane] = 0u;
 #pragma unroll 1
         for (int sl = 0; sl < PL::NLR + PL::NLS; ++sl) sm->pm[sl][lane] = 0u;
-        sm->inact[lane] = 0;
 #pragma unroll 1
         for (int i = lane; i < N / 4; i += 32) reinterpret_cast<uint32_t*>(sm->fst)[i] = 0x7f7f7f7fu;
         __syncwarp();
