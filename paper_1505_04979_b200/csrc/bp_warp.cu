@@ -102,7 +102,6 @@ struct Plan {
 template <int M>
 struct WarpSmem {
     using PL = Plan<M>;
-    float4 R0p[PL::P / 4][32];             // channel LLRs, lane-private pass-0 layout
     float X[PL::Q - 1][PL::NX];            // pass boundaries: R(e) then L(e), padded rows
     float4 Ls[PL::NLS][PL::P / 4][32];     // lane-private L slots (last pass, n=1024)
     float4 LM[PL::P / 4][32];              // L(m), lane-private, last-pass layout
@@ -188,6 +187,7 @@ struct Dec {
     static constexpr int N = PL::N, P = PL::P, K = PL::K, Q = PL::Q, NW = PL::NW;
 
     WarpSmem<M>* sm;
+    float4* r0g;  // this warp's channel LLRs in global scratch, lane-private pass-0 layout
     const DecodeArgs* a;
     int lane;
     float alpha;
@@ -922,7 +922,7 @@ struct Dec {
             if constexpr (KIND != 0) xq = 0u;
 #pragma unroll
             for (int c = 0; c < P / 4; ++c) {
-                const float4 v = sm->R0p[c][lane];
+                const float4 v = r0g[c * 32 + lane];
                 R[4 * c] = v.x;
                 R[4 * c + 1] = v.y;
                 R[4 * c + 2] = v.z;
@@ -1012,6 +1012,7 @@ struct Dec {
 
     __device__ __forceinline__ void run(const DecodeArgs& args, WarpSmem<M>* s, int ln) {
         a = &args;
+        r0g = reinterpret_cast<float4*>(args.r0s) + (long long)blockIdx.x * (N / 4);
         sm = s;
         lane = ln;
         alpha = args.alpha;
@@ -1136,7 +1137,7 @@ struct Dec {
     __device__ __forceinline__ bool load_frame(long long f) {
         const float4* src = reinterpret_cast<const float4*>(a->llr + f * (long long)N);
         bool bad = false;
-        float* r0 = reinterpret_cast<float*>(sm->R0p);
+        float* r0 = sm->X[0];  // staging (X is re-initialised after the frame load)
 #pragma unroll 4
         for (int i = 0; i < P / 4; ++i) {
             const float4 v = __ldcs(src + lane + 32 * i);
@@ -1149,6 +1150,11 @@ struct Dec {
                 r0[((j >> 2) * 32 + l2) * 4 + (j & 3)] = __fadd_rn(e[k], 0.0f);  // -0 -> +0
             }
         }
+        __syncwarp();
+        // each lane keeps its own slots: it is the only reader (stage 0)
+#pragma unroll
+        for (int c = 0; c < P / 4; ++c) r0g[c * 32 + lane] = reinterpret_cast<const float4*>(r0)[c * 32 + lane];
+        __syncwarp();  // X is overwritten next
         return !__any_sync(kFull, bad);
     }
 

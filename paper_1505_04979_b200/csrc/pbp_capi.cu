@@ -91,6 +91,7 @@ struct pbp_ctx {
     DevBuf<unsigned long long> ctl;  // [0] warp queue, [1] generic queue, [2] list length
     DevBuf<long long> list;
     DevBuf<float> scratch;
+    DevBuf<float> r0s;                 // warp kernel: per-CTA channel LLRs
     DevBuf<unsigned long long> counters;
     // host-API staging
     DevBuf<float> llr;
@@ -202,6 +203,8 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, cudaStream_t st) {
         a.list_mode = 0;
         const int per_sm = std::max(1, pbp::warp_blocks_per_sm(ctx->m, r.kind));
         const long long grid = std::min<long long>((long long)per_sm * ctx->sm_count, r.frames);
+        if ((rc = ctx->r0s.ensure((size_t)(grid * ctx->n)))) return rc;
+        a.r0s = ctx->r0s.p;
         cudaError_t e = pbp::launch_warp(a, (int)grid, st);
         if (e != cudaSuccess) return cuda_fail(e, "bp_warp_kernel launch");
         ctx->last_launches += 1;
@@ -298,6 +301,7 @@ int pbp_ctx_destroy(pbp_ctx* ctx) {
     ctx->ctl.release();
     ctx->list.release();
     ctx->scratch.release();
+    ctx->r0s.release();
     ctx->counters.release();
     ctx->llr.release();
     ctx->ubits.release();

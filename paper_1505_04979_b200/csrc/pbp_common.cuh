@@ -47,6 +47,7 @@ struct DecodeArgs {
     long long* list;
     unsigned long long* list_len;
     int list_mode;
+    float* r0s;                       // warp kernel: per-CTA channel LLRs (n floats each)
     float* scratch;                   // generic kernel: per-CTA message arrays
     long long scratch_stride;         // floats per CTA
 };

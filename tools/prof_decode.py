@@ -23,6 +23,9 @@ P._check(P.lib.pbp_generate_device(ctx.handle, C.byref(cs), C.c_uint64(2), 0, a.
                                    P._abi.f32p(llr.data_ptr()), None, P._abi.u32p(u.data_ptr()), None))
 ctx.synchronize()
 kind = P.DecoderKind.parse(a.kind)
+_sm, _w = C.c_int32(), C.c_int32()
+P.lib.pbp_kernel_info(a.n, kind, C.byref(_sm), C.byref(_w))
+print(f"warp kernel: {_sm.value} B shared, {_w.value} warps/SM")
 for r in range(a.reps):
     cnt.zero_()
     torch.cuda.synchronize()
