@@ -1211,8 +1211,13 @@ struct Dec {
     }
 };
 
+// resident warps per SM the register budget is sized for (per 16K-register
+// SM partition: 2 warps at <= 256 registers, 3 at <= 168, 4 at <= 128)
+template <int M>
+constexpr int kMinWarps = M >= 10 ? 1 : (M == 9 ? 12 : (M == 8 ? 16 : 20));
+
 template <int M, int KIND>
-__global__ void __launch_bounds__(32) bp_warp_kernel(DecodeArgs a) {
+__global__ void __launch_bounds__(32, kMinWarps<M>) bp_warp_kernel(DecodeArgs a) {
     extern __shared__ __align__(16) unsigned char wsm[];
     Dec<M, KIND> dec;
     dec.run(a, reinterpret_cast<WarpSmem<M>*>(wsm), threadIdx.x & 31);
