@@ -998,7 +998,25 @@ struct Dec {
         }
     }
 
+    // Pinned G-check (csfg_freeze.cpp:128-140, bp_core.cpp:104-110): x_hat of
+    // stage 0 == polar_transform(u_hat'), u_hat' = u_hat with frozen rows 0
+    // and rows < pin from decided_u. Exact filter first: the parity of x_hat
+    // over each row class mod 32 (one bit per lane of the pass-0 layout) must
+    // equal that of G(u_hat'), which is the in-word transform of u_hat' rows
+    // 0..31 alone (a row i >= 32 lies above an even number of rows of each
+    // class). Those rows are known without the sweep's R when they are all
+    // frozen or decided; a mismatch proves x_hat != G(u_hat').
     __device__ __forceinline__ bool gcheck(int pin) {
+        const uint32_t free0 = ~sm->frz[0] & ~low_mask(pin < 32 ? pin : 32);
+        if (free0 == 0u) {
+            const uint32_t cls = __ballot_sync(kFull, __popc(xq) & 1);
+            const uint32_t u0 = pin > 0 ? sm->dec_u[0] & low_mask(pin < 32 ? pin : 32) : 0u;
+            if (cls != word_transform(u0, 32)) return false;
+        }
+        return gcheck_full(pin);
+    }
+
+    __device__ __forceinline__ bool gcheck_full(int pin) {
         uint32_t uw = u_words(pin);
         uw = word_transform(uw, 32);
 #pragma unroll
