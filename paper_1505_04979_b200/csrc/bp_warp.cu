@@ -573,80 +573,75 @@ struct Dec {
         }
     }
 
-    // Late walk. Lane t < NL takes stage SL + t: the sign bits x of rows
-    // P*L1 + i (i < 2P) after that stage, their transform u inside each
-    // 2^g-row block, and a bitmap of rejected blocks (bit at each block's first
-    // row), so a round of the walk is one bit test per lane. A committing lane
-    // keeps its block start in lA (a stage commits at most once per iteration).
-    using WT = typename std::conditional<(P == 32), unsigned long long, uint32_t>::type;
-    __device__ __forceinline__ void walk_late(WT& xw, WT& uw, int& lA, uint32_t& cmask) {
+    // Late walk over the last-pass stages. Every candidate block lies in the
+    // window of 2*W1 <= 32 rows from A5 = frontier rounded down to the first
+    // last-pass block size W1 (after a commit the blocks shrink). x_t = sign
+    // bits of the window after stage SL + t (one ballot); lane t transforms x_t
+    // inside its 2^g-row blocks and marks the rejected ones (bit at the block's
+    // first row); every lane then runs the stage loop as a straight scan.
+    struct LastWalk {
+        int A5;               // window start
+        uint32_t x[PL::NL];   // window sign bits per last-pass stage (uniform)
+        int A[PL::NL];        // block start of stage SL + t's candidate
+        uint32_t xl, ul;      // lane t: x_hat / u_hat bits of the window at stage SL + t
+        int Al;               // lane t: A[t]
+        uint32_t cmask;       // bit t: stage SL + t committed
+    };
+    __device__ __forceinline__ void walk_late(LastWalk& w) {
         constexpr int SL = PL::SL, NL = PL::NL;
+        constexpr int W1 = 1 << (M - 1 - SL);
         __syncwarp();  // rs rows
-        cmask = 0u;
+        w.cmask = 0u;
         if (done_) return;
-        WT wv = 0;
+        w.A5 = frontier & ~(W1 - 1);
+        const int off = w.A5 - P * L1;  // window offset in the two stored lanes' rows
+        uint32_t xl = 0u;
 #pragma unroll
         for (int t = 0; t < NL; ++t) {
-            WT w;
-            if constexpr (P == 32) {
-                const uint32_t lo = __ballot_sync(kFull, __float_as_int(sm->rs[t][0][lane]) < 0);
-                const uint32_t hi = __ballot_sync(kFull, __float_as_int(sm->rs[t][1][lane]) < 0);
-                w = (WT)lo | ((WT)hi << 32);
-            } else {
-                const float* f = &sm->rs[t][0][0];
-                const float v = lane < 2 * P ? f[lane] : 0.f;
-                w = __ballot_sync(kFull, lane < 2 * P && __float_as_int(v) < 0);
-            }
-            if (lane == t) wv = w;
+            const float v = lane < 2 * W1 ? (&sm->rs[t][0][0])[off + lane] : 0.f;
+            const uint32_t xt = __ballot_sync(kFull, lane < 2 * W1 && __float_as_int(v) < 0);
+            w.x[t] = xt;
+            if (lane == t) xl = xt;
         }
-        const int row0 = P * L1;
-        const int g = M - 1 - (SL + lane);  // this lane's stage (lane < NL)
-        xw = wv;
-        uw = wv;
-        WT viol;
+        uint32_t viol;
         {
-            const int w0 = row0 >> 5;
-            if constexpr (P == 32) {
-                viol = (WT)sm->frz[w0] | ((WT)(w0 + 1 < NW ? sm->frz[w0 + 1] : 0u) << 32);
-            } else {
-                const unsigned long long f2 =
-                    (unsigned long long)sm->frz[w0] | ((unsigned long long)(w0 + 1 < NW ? sm->frz[w0 + 1] : 0u) << 32);
-                viol = (WT)(f2 >> (row0 & 31));
-            }
+            const int w0 = w.A5 >> 5;
+            const unsigned long long f2 =
+                (unsigned long long)sm->frz[w0] | ((unsigned long long)(w0 + 1 < NW ? sm->frz[w0 + 1] : 0u) << 32);
+            viol = (uint32_t)(f2 >> (w.A5 & 31));
         }
+        const int g = M - 1 - (SL + lane);  // lane t < NL: its stage's block bits
+        uint32_t u = xl;
 #pragma unroll
-        for (int tp = 0; tp < K - 1; ++tp) {
-            const WT jm = (WT)jmask(tp) | ((WT)jmask(tp) << (sizeof(WT) * 8 - 32));
-            if (tp < g) uw ^= (uw >> (1 << tp)) & jm;
-        }
-        viol &= uw;
+        for (int tp = 0; tp < K - 1; ++tp)
+            if (tp < g) u ^= (u >> (1 << tp)) & jmask(tp);
+        w.xl = xl;
+        w.ul = u;
+        viol &= u;
 #pragma unroll
         for (int tp = 0; tp < K - 1; ++tp)
             if (tp < g) viol |= viol >> (1 << tp);
-        int s_next = SL;
-#pragma unroll 1
-        for (;;) {
-            bool acc = false;
-            if (lane < NL && SL + lane >= s_next) {
-                const int A = (frontier >> g) << g;
-                acc = !((viol >> (A - row0)) & 1u);
-            }
-            const uint32_t am = __ballot_sync(kFull, acc);
-            if (!am) break;
-            const int t = __ffs(am) - 1;
+        // the reference's stage loop over the last pass
+        int F = frontier;
+        bool done = false;
+#pragma unroll
+        for (int t = 0; t < NL; ++t) {
+            const uint32_t vt = __shfl_sync(kFull, viol, t);
             const int gt = M - 1 - (SL + t);
-            const int A = (frontier >> gt) << gt;
-            if (lane == t) lA = A;
-            cmask |= 1u << t;
-            frontier = A + (1 << gt);
-            if (frontier >= N) {
-                s_last_ = SL + t;
-                done_ = true;
-                break;
+            const int A = (F >> gt) << gt;
+            w.A[t] = A;
+            if (lane == t) w.Al = A;
+            if (!done && !((vt >> (A - w.A5)) & 1u)) {
+                w.cmask |= 1u << t;
+                F = A + (1 << gt);
+                if (F >= N) {
+                    s_last_ = SL + t;
+                    done = true;
+                }
             }
-            s_next = SL + t + 1;
-            if (s_next >= M) break;
         }
+        frontier = F;
+        done_ = done;
     }
 
     // after the sweep: late walk, side effects, stage_pass counts of stages
@@ -655,13 +650,11 @@ struct Dec {
     // pinned G-check).
     __device__ __forceinline__ bool finish_iter() {
         PBP_T0(tw);
-        WT xw, uw;
-        int lA = 0;
-        uint32_t cmask;
-        walk_late(xw, uw, lA, cmask);
+        LastWalk w;
+        walk_late(w);
         PBP_T1(tw, 3);
         PBP_T0(ta);
-        if (nce_ | cmask) apply_commits(xw, uw, lA, cmask);
+        if (nce_ | w.cmask) apply_commits(w);
         PBP_T1(ta, 4);
         const int v = lane <= s_last_ ? (N >> 1) - inact : 0;
         act += __reduce_add_sync(kFull, v);
@@ -673,7 +666,7 @@ struct Dec {
     // event log. Commits of the early walk one after the other with the whole
     // warp (their blocks span lanes); last-pass commits one per lane (blocks
     // are disjoint, their L(S+1) are different arrays).
-    __device__ __forceinline__ void apply_commits(WT xw, WT uw, int lA, uint32_t cmask) {
+    __device__ __forceinline__ void apply_commits(const LastWalk& w) {
         constexpr uint32_t REGM = mask_of(0), SMEMM = mask_of(1);
         const int nce = nce_, fr_start = fr_start_;
         __syncwarp();
@@ -776,36 +769,48 @@ struct Dec {
             }
             ++nev;
         }
-        if (cmask) apply_last(xw, uw, lA, cmask, nce, fr_start, dinact);
+        if (w.cmask) apply_last(w, nce, fr_start, dinact);
         if (lane < M) inact += dinact;
         __syncwarp();
     }
 
-    // last-pass commits: lane t applies its stage's (cmask bit t)
-    __device__ __forceinline__ void apply_last(WT xw, WT uw, int lA, uint32_t cmask, int nce, int fr_start,
-                                               int& dinact) {
+    // Last-pass commits (cmask bit t: stage SL + t), all inside the window:
+    // lane i takes row A5 + i (its block's stage and x_hat bit: saturation,
+    // freeze_stage); lane t takes stage SL + t's commit (decided_u, protection
+    // mask, event).
+    __device__ __forceinline__ void apply_last(const LastWalk& w, int nce, int fr_start, int& dinact) {
         constexpr uint32_t REGM = mask_of(0), SMEMM = mask_of(1);
-        constexpr int SL = PL::SL;
-        const bool mine = (cmask >> lane) & 1u;
+        constexpr int SL = PL::SL, NL = PL::NL;
+        const uint32_t cmask = w.cmask;
         // inactive top rows: a stage-S block of sz rows has sz/2 top rows at
         // every later stage (stages are distinct and increasing in one walk)
         const uint32_t cm = cmask << SL;
         if (lane < M) dinact += (int)((__brev(cm & ((1u << lane) - 1u)) >> (32 - M)) >> 1);
+        const int r = w.A5 + lane;
+        int Sr = -1;
+        uint32_t xbit = 0u;
+#pragma unroll
+        for (int t = 0; t < NL; ++t) {
+            const int gt = M - 1 - (SL + t);
+            if (((cmask >> t) & 1u) && r >= w.A[t] && r < w.A[t] + (1 << gt)) {
+                Sr = SL + t;
+                xbit = (w.x[t] >> lane) & 1u;
+            }
+        }
+        int fo = kNotFrozen;
+        if (Sr >= 0) fo = sm->fst[r];
         if (nce == 0) {
             // the first commit of the iteration may re-cover decided rows
-            // [A, fr_start) (< 32 of them): those already inactive at a stage
-            // s2 > S0 under their old freeze_stage are not counted twice
+            // [A0, fr_start): those already inactive at a stage s2 > S0 under
+            // their old freeze_stage are not counted twice
             const int t0 = __ffs(cmask) - 1;
             const int S0 = SL + t0;
-            const int A0 = __shfl_sync(kFull, lA, t0);
-            if (A0 < fr_start) {
-                const int r = A0 + lane;
+            if (__any_sync(kFull, Sr >= 0 && r < fr_start)) {
                 uint32_t was = 0u;
-                if (r < fr_start) {
-                    const int fo = sm->fst[r];
-#pragma unroll
-                    for (int s2 = 1; s2 < M; ++s2)
-                        if (s2 > S0 && fo < s2 && !((r >> (M - 1 - s2)) & 1)) was |= 1u << s2;
+                if (Sr >= 0 && r < fr_start) {
+                    const int lo = fo > S0 ? fo : S0;  // s2 > max(fo, S0)
+                    const uint32_t top = __brev(~(uint32_t)r) >> (32 - M);  // bit s2: row is top at s2
+                    was = top & ~((2u << lo) - 1u);
                 }
 #pragma unroll
                 for (int s2 = 1; s2 < M; ++s2) {
@@ -813,59 +818,44 @@ struct Dec {
                     if (lane == s2) dinact -= c;
                 }
             }
-            __syncwarp();  // freeze_stage reads before the writes below
         }
-        uint32_t myprot = 0u;
-        if (mine) {
-            const int S = SL + lane;
-            const int g = M - 1 - S, W = 1 << g;
-            const int A = lA;
-            const uint32_t wm = (1u << W) - 1u;
-            const int off = A - P * L1;
-            const uint32_t xb = (uint32_t)(xw >> off) & wm, ub = (uint32_t)(uw >> off) & wm;
-            const int owner = A / P, j0 = A % P;  // last-pass layout: row = P*lane + j
-            const int T = S + 1;
-            // 1. saturate / protect L(S+1) (csfg_freeze.cpp:84-86)
+        // 1. saturate L(S+1) (csfg_freeze.cpp:84-86), 3. freeze_stage (:86)
+        if (Sr >= 0) {
+            const int T = Sr + 1;
+            const int owner = r / P, j = r % P;  // last-pass layout: row = P*lane + j
             if (T == M || ((SMEMM >> T) & 1u)) {
                 float* base = (T == M) ? reinterpret_cast<float*>(&sm->LM[0][0])
                                        : reinterpret_cast<float*>(&sm->Ls[__popc(SMEMM & ((1u << T) - 1u))][0][0]);
-                if (W >= 4) {
-#pragma unroll 1
-                    for (int i = 0; i < W; i += 4)
-                        reinterpret_cast<float4*>(base)[((j0 + i) >> 2) * 32 + owner] = make_float4(
-                            ((xb >> i) & 1u) ? -kCap : kCap, ((xb >> (i + 1)) & 1u) ? -kCap : kCap,
-                            ((xb >> (i + 2)) & 1u) ? -kCap : kCap, ((xb >> (i + 3)) & 1u) ? -kCap : kCap);
-                } else {
-#pragma unroll 1
-                    for (int i = 0; i < W; ++i) {
-                        const int j = j0 + i;
-                        base[((j >> 2) * 32 + owner) * 4 + (j & 3)] = ((xb >> i) & 1u) ? -kCap : kCap;
-                    }
-                }
-                if (T != M) {
+                base[((j >> 2) * 32 + owner) * 4 + (j & 3)] = xbit ? -kCap : kCap;
+            }
+            sm->fst[r] = (uint8_t)Sr;
+        }
+        // 2. decided_u (:87), protection masks, event log (:91-92): lane t
+        uint32_t myprot = 0u;
+        if ((cmask >> lane) & 1u) {
+            const int S = SL + lane;
+            const int g = M - 1 - S, W = 1 << g;
+            const int A = w.Al;
+            const uint32_t xt = w.xl;
+            const uint32_t wm = (1u << W) - 1u;
+            const int o = A - w.A5;
+            const uint32_t xb = (xt >> o) & wm, ub = (w.ul >> o) & wm;
+            atomicAnd(&sm->dec_u[A >> 5], ~(wm << (A & 31)));
+            atomicOr(&sm->dec_u[A >> 5], ub << (A & 31));
+            const int owner = A / P, j0 = A % P;
+            const int T = S + 1;
+            if (T != M) {
+                if ((SMEMM >> T) & 1u) {
                     const int ps = PL::NLR + __popc(SMEMM & ((1u << T) - 1u));
                     sm->pm[ps][owner] |= wm << j0;
                     myprot = 1u << ps;
+                } else {  // register array in the last-pass layout
+                    const int sl = __popc(REGM & ((1u << T) - 1u));
+                    sm->pm[sl][owner] |= wm << j0;
+                    sm->ss[sl][owner] = (sm->ss[sl][owner] & ~(wm << j0)) | (xb << j0);
+                    myprot = 1u << sl;
                 }
-            } else {  // register array in the last-pass layout
-                const int sl = __popc(REGM & ((1u << T) - 1u));
-                sm->pm[sl][owner] |= wm << j0;
-                sm->ss[sl][owner] = (sm->ss[sl][owner] & ~(wm << j0)) | (xb << j0);
-                myprot = 1u << sl;
             }
-            // 2. decided_u (csfg_freeze.cpp:87)
-            atomicAnd(&sm->dec_u[A >> 5], ~(wm << (A & 31)));
-            atomicOr(&sm->dec_u[A >> 5], ub << (A & 31));
-            // 3. freeze_stage over the block (csfg_freeze.cpp:86)
-            if (W >= 4) {
-                const uint32_t w4 = 0x01010101u * (uint32_t)S;
-#pragma unroll 1
-                for (int i = 0; i < W; i += 4) *reinterpret_cast<uint32_t*>(&sm->fst[A + i]) = w4;
-            } else {
-                sm->fst[A] = (uint8_t)S;
-                if (W == 2) sm->fst[A + 1] = (uint8_t)S;
-            }
-            // 4. event log (csfg_freeze.cpp:91-92)
             const int e_ix = nev + __popc(cmask & ((1u << lane) - 1u));
             if (a->events && e_ix < a->ev_cap) {
                 int* e = a->events + ((long long)frame_ * a->ev_cap + e_ix) * 5;
