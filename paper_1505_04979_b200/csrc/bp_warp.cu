@@ -1050,7 +1050,7 @@ struct Dec {
             if (!load_frame(f)) {
                 if (lane == 0) {
                     const unsigned long long slot = atomicAdd(args.list_len, 1ull);
-                    args.list[slot] = f;
+                    args.list[slot] = f + args.frame_base;
                 }
                 continue;
             }

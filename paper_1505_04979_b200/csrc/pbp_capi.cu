@@ -77,22 +77,34 @@ struct DevBuf {
 
 }  // namespace
 
+// Launch resources of one in-flight decode: work queue, re-route list and
+// scratch are per launch, so decodes on different streams need their own.
+struct DecodeSlot {
+    cudaStream_t stream = nullptr;     // slot 0: the context stream
+    DevBuf<unsigned long long> ctl;    // [0] warp queue, [1] generic queue, [2] list length
+    DevBuf<long long> list;
+    DevBuf<float> scratch;             // generic kernel: per-CTA message arrays
+    DevBuf<float> r0s;                 // warp kernel: per-CTA channel LLRs
+};
+constexpr int kSlots = 3;
+
 struct pbp_ctx {
     int device = 0;
     int sm_count = 0;
     cudaStream_t stream = nullptr;
+    DecodeSlot slot[kSlots];
     // code tables
     std::vector<uint8_t> code_key;
     int n = 0, m = 0, k = 0;
     DevBuf<uint32_t> frozen_bits;
     DevBuf<uint8_t> frozen_rows;
     DevBuf<int> info_rows;
-    // work queue + re-route list
-    DevBuf<unsigned long long> ctl;  // [0] warp queue, [1] generic queue, [2] list length
-    DevBuf<long long> list;
-    DevBuf<float> scratch;
-    DevBuf<float> r0s;                 // warp kernel: per-CTA channel LLRs
     DevBuf<unsigned long long> counters;
+    DevBuf<unsigned long long> rerouted;  // per launch of the last call: frames re-routed
+    int n_launch_sets = 0;
+    long long rerouted_host = -1;         // the last call's count when known on the host
+    DevBuf<long long> blist;              // batch-wide re-route list (pipelined host batch)
+    DevBuf<unsigned long long> bctl;      // [0] its length, [1] generic queue
     // host-API staging
     DevBuf<float> llr;
     DevBuf<uint32_t> ubits, truth;
@@ -162,17 +174,55 @@ struct DecodeReq {
     const uint32_t* truth = nullptr;
     unsigned long long* counters = nullptr;
     bool force_generic = false;
+    // fast path: re-routed frames go to this list (indices + frame_base) and
+    // the caller runs the generic pass later (run_generic_list)
+    long long* list = nullptr;
+    unsigned long long* list_len = nullptr;
+    long long frame_base = 0;
 };
 
-// Launch the decode of `frames` frames already on the device.
-int run_decode(pbp_ctx* ctx, const DecodeReq& r, cudaStream_t st) {
+// Start of an API call that launches decodes: launch statistics restart.
+int begin_call(pbp_ctx* ctx, int max_sets) {
+    ctx->last_launches = 0;
+    ctx->n_launch_sets = 0;
+    ctx->rerouted_host = -1;
+    return ctx->rerouted.ensure((size_t)std::max(max_sets, 16));
+}
+
+// Grid of the generic kernel: every frame when it decodes alone, the
+// re-routed frames (at most one per SM at a time) after the warp kernel;
+// bounded by 1 GiB of per-CTA scratch.
+long long generic_grid(const pbp_ctx* ctx, long long frames, bool fast) {
+    const long long gfm = fast ? std::min<long long>(frames, ctx->sm_count) : frames;
+    const long long stride = pbp::generic_scratch_floats(ctx->n, ctx->m);
+    long long grid = std::min<long long>(gfm, (long long)ctx->sm_count * 4);
+    const long long max_scratch_floats = 1ll << 28;  // 1 GiB
+    return std::max<long long>(1, std::min<long long>(grid, max_scratch_floats / stride));
+}
+
+// Size a slot's buffers for decodes of up to `frames` frames (before any
+// asynchronous work is queued: reallocation synchronises the device).
+int size_slot(pbp_ctx* ctx, DecodeSlot& s, int kind, long long frames) {
+    int rc;
+    if ((rc = s.ctl.ensure(4)) || (rc = s.list.ensure(std::max<long long>(frames, 1)))) return rc;
+    if (pbp::warp_kernel_supported(ctx->m)) {
+        const int per_sm = std::max(1, pbp::warp_blocks_per_sm(ctx->m, kind));
+        const long long grid = std::min<long long>((long long)per_sm * ctx->sm_count, std::max<long long>(frames, 1));
+        if ((rc = s.r0s.ensure((size_t)(grid * ctx->n)))) return rc;
+    }
+    const bool fast = !ctx->force_generic && pbp::warp_kernel_supported(ctx->m);
+    return s.scratch.ensure((size_t)generic_grid(ctx, frames, fast) * pbp::generic_scratch_floats(ctx->n, ctx->m));
+}
+
+// Launch the decode of `frames` frames already on the device, with slot s's
+// launch resources, on stream st.
+int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st) {
     if (r.kind < 0 || r.kind > 2) return fail(PBP_EINVAL, "unknown decoder kind");
     if (r.frames < 0) return fail(PBP_EINVAL, "frames < 0");
-    ctx->last_launches = 0;
     if (r.frames == 0) return PBP_OK;
     int rc;
-    if ((rc = ctx->ctl.ensure(4))) return rc;
-    PBP_CUDA(cudaMemsetAsync(ctx->ctl.p, 0, 4 * sizeof(unsigned long long), st));
+    if ((rc = size_slot(ctx, s, r.kind, r.frames))) return rc;
+    PBP_CUDA(cudaMemsetAsync(s.ctl.p, 0, 4 * sizeof(unsigned long long), st));
     pbp::DecodeArgs a{};
     a.n = ctx->n;
     a.m = ctx->m;
@@ -192,37 +242,79 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, cudaStream_t st) {
     a.ev_cap = r.ev_cap;
     a.truth_u = r.truth;
     a.counters = r.counters;
-    a.list_len = ctx->ctl.p + 2;
+    a.list_len = s.ctl.p + 2;
 
     const bool fast = !r.force_generic && !ctx->force_generic && pbp::warp_kernel_supported(ctx->m);
-    long long generic_frames_max = r.frames;
     if (fast) {
-        if ((rc = ctx->list.ensure(r.frames))) return rc;
-        a.list = ctx->list.p;
-        a.queue = ctx->ctl.p + 0;
+        a.list = r.list ? r.list : s.list.p;
+        if (r.list_len) a.list_len = r.list_len;
+        a.frame_base = r.frame_base;
+        a.queue = s.ctl.p + 0;
         a.list_mode = 0;
         const int per_sm = std::max(1, pbp::warp_blocks_per_sm(ctx->m, r.kind));
         const long long grid = std::min<long long>((long long)per_sm * ctx->sm_count, r.frames);
-        if ((rc = ctx->r0s.ensure((size_t)(grid * ctx->n)))) return rc;
-        a.r0s = ctx->r0s.p;
+        a.r0s = s.r0s.p;
         cudaError_t e = pbp::launch_warp(a, (int)grid, st);
         if (e != cudaSuccess) return cuda_fail(e, "bp_warp_kernel launch");
         ctx->last_launches += 1;
+        if (r.list) return PBP_OK;  // the caller runs the generic pass over the shared list
         // frames the fast kernel re-routed (|LLR| beyond the clamp-free bound)
         a.list_mode = 1;
-        generic_frames_max = std::min<long long>(r.frames, ctx->sm_count);
     } else {
         a.list = nullptr;
         a.list_mode = 0;
     }
-    a.queue = ctx->ctl.p + 1;
+    a.queue = s.ctl.p + 1;
     // generic kernel: bounded grid, per-CTA scratch
     const long long stride = pbp::generic_scratch_floats(ctx->n, ctx->m);
-    long long grid = std::min<long long>(generic_frames_max, (long long)ctx->sm_count * 4);
-    const long long max_scratch_floats = 1ll << 28;  // 1 GiB
-    grid = std::max<long long>(1, std::min<long long>(grid, max_scratch_floats / stride));
-    if ((rc = ctx->scratch.ensure((size_t)(grid * stride)))) return rc;
-    a.scratch = ctx->scratch.p;
+    const long long grid = generic_grid(ctx, r.frames, fast);
+    if ((rc = s.scratch.ensure((size_t)(grid * stride)))) return rc;
+    a.scratch = s.scratch.p;
+    a.scratch_stride = stride;
+    cudaError_t e = pbp::launch_generic(a, (int)grid, st);
+    if (e != cudaSuccess) return cuda_fail(e, "bp_generic_kernel launch");
+    ctx->last_launches += 1;
+    if (ctx->n_launch_sets < (int)ctx->rerouted.cap) {
+        PBP_CUDA(cudaMemcpyAsync(ctx->rerouted.p + ctx->n_launch_sets, s.ctl.p + 2, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToDevice, st));
+        ctx->n_launch_sets += 1;
+    }
+    return PBP_OK;
+}
+
+// The generic kernel over a re-route list (frame indices relative to r.llr
+// and r's output arrays).
+int run_generic_list(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st, long long listed) {
+    int rc;
+    if ((rc = s.ctl.ensure(4))) return rc;
+    PBP_CUDA(cudaMemsetAsync(s.ctl.p, 0, 4 * sizeof(unsigned long long), st));
+    pbp::DecodeArgs a{};
+    a.n = ctx->n;
+    a.m = ctx->m;
+    a.kind = r.kind;
+    a.max_iter = r.max_iter;
+    a.alpha = r.alpha;
+    a.frozen_bits = ctx->frozen_bits.p;
+    a.frozen_rows = ctx->frozen_rows.p;
+    a.llr = r.llr;
+    a.frames = r.frames;
+    a.u_bits = r.u_bits;
+    a.iters = r.iters;
+    a.pe = r.pe;
+    a.stop = r.stop;
+    a.nev = r.nev;
+    a.events = r.events;
+    a.ev_cap = r.ev_cap;
+    a.truth_u = r.truth;
+    a.counters = r.counters;
+    a.list = r.list;
+    a.list_len = r.list_len;
+    a.list_mode = 1;
+    a.queue = s.ctl.p + 1;
+    const long long stride = pbp::generic_scratch_floats(ctx->n, ctx->m);
+    const long long grid = generic_grid(ctx, std::max<long long>(1, listed), false);
+    if ((rc = s.scratch.ensure((size_t)(grid * stride)))) return rc;
+    a.scratch = s.scratch.p;
     a.scratch_stride = stride;
     cudaError_t e = pbp::launch_generic(a, (int)grid, st);
     if (e != cudaSuccess) return cuda_fail(e, "bp_generic_kernel launch");
@@ -283,10 +375,16 @@ int pbp_ctx_create(int device, pbp_ctx** out) {
     ctx->device = device;
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    for (int i = 1; i < kSlots && e == cudaSuccess; ++i)
+        e = cudaStreamCreateWithFlags(&ctx->slot[i].stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
+        for (int i = 1; i < kSlots; ++i)
+            if (ctx->slot[i].stream) cudaStreamDestroy(ctx->slot[i].stream);
+        if (ctx->stream) cudaStreamDestroy(ctx->stream);
         delete ctx;
         return cuda_fail(e, "cudaStreamCreate");
     }
+    ctx->slot[0].stream = ctx->stream;
     *out = ctx;
     return PBP_OK;
 }
@@ -298,10 +396,19 @@ int pbp_ctx_destroy(pbp_ctx* ctx) {
     ctx->frozen_bits.release();
     ctx->frozen_rows.release();
     ctx->info_rows.release();
-    ctx->ctl.release();
-    ctx->list.release();
-    ctx->scratch.release();
-    ctx->r0s.release();
+    for (int i = 0; i < kSlots; ++i) {
+        if (i > 0 && ctx->slot[i].stream) {
+            cudaStreamSynchronize(ctx->slot[i].stream);
+            cudaStreamDestroy(ctx->slot[i].stream);
+        }
+        ctx->slot[i].ctl.release();
+        ctx->slot[i].list.release();
+        ctx->slot[i].scratch.release();
+        ctx->slot[i].r0s.release();
+    }
+    ctx->rerouted.release();
+    ctx->blist.release();
+    ctx->bctl.release();
     ctx->counters.release();
     ctx->llr.release();
     ctx->ubits.release();
@@ -345,11 +452,13 @@ int pbp_last_launch_info(pbp_ctx* ctx, int32_t* launches, int64_t* rerouted) {
     if (launches) *launches = ctx->last_launches;
     if (rerouted) {
         *rerouted = 0;
-        if (ctx->ctl.p) {
-            unsigned long long v = 0;
-            PBP_CUDA(cudaStreamSynchronize(ctx->stream));
-            PBP_CUDA(cudaMemcpy(&v, ctx->ctl.p + 2, sizeof(v), cudaMemcpyDeviceToHost));
-            *rerouted = (int64_t)v;
+        if (ctx->rerouted_host >= 0) {
+            *rerouted = ctx->rerouted_host;
+        } else if (ctx->n_launch_sets > 0) {
+            std::vector<unsigned long long> v(ctx->n_launch_sets);
+            for (int i = 0; i < kSlots; ++i) PBP_CUDA(cudaStreamSynchronize(ctx->slot[i].stream));
+            PBP_CUDA(cudaMemcpy(v.data(), ctx->rerouted.p, v.size() * sizeof(v[0]), cudaMemcpyDeviceToHost));
+            for (unsigned long long x : v) *rerouted += (int64_t)x;
         }
     }
     return PBP_OK;
@@ -427,7 +536,8 @@ int pbp_decode_batch_device(pbp_ctx* ctx, const pbp_code* code, int decoder, con
         r.stop = out_dev->stop;
         r.nev = out_dev->n_events;
     }
-    return run_decode(ctx, r, pick(ctx, stream));
+    if ((rc = begin_call(ctx, 1))) return rc;
+    return run_decode(ctx, r, ctx->slot[0], pick(ctx, stream));
 }
 
 int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs,
@@ -442,30 +552,100 @@ int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
         (rc = ctx->iters.ensure(frames)) || (rc = ctx->pe.ensure(frames)) ||
         (rc = ctx->stop.ensure(frames)) || (rc = ctx->nev.ensure(frames)))
         return rc;
+    // Chunks round-robin over the slots' streams: the host->device copy of one
+    // chunk overlaps the decode of the others (and a decode's tail overlaps
+    // the next chunk's launch). A small first chunk starts the GPU early.
+    constexpr long long kChunkMin = 16384, kFirst = 4096;
+    std::vector<long long> bounds{0};
+    if (frames >= 2 * kChunkMin) {
+        bounds.push_back(kFirst);
+        const long long rest = frames - kFirst;
+        const long long nrest = std::min<long long>(7, rest / kChunkMin);
+        for (long long i = 1; i <= nrest; ++i) bounds.push_back(kFirst + rest * i / nrest);
+    } else {
+        bounds.push_back(frames);
+    }
+    const int nchunks = (int)bounds.size() - 1;
+    long long per = 0;
+    for (int c = 0; c < nchunks; ++c) per = std::max(per, bounds[c + 1] - bounds[c]);
+    if ((rc = begin_call(ctx, nchunks))) return rc;
+    for (int i = 0; i < std::min(nchunks, kSlots); ++i)
+        if ((rc = size_slot(ctx, ctx->slot[i], decoder, per))) return rc;
+    // frames re-routed by any chunk's fast kernel: one batch-wide list, decoded
+    // by a single generic pass once the pipeline has drained (rare; no generic
+    // launch between the chunks, whose CTAs would stall the other streams)
+    const bool fast = !ctx->force_generic && pbp::warp_kernel_supported(ctx->m);
+    if (fast) {
+        if ((rc = ctx->blist.ensure(std::max<long long>(frames, 1))) || (rc = ctx->bctl.ensure(2))) return rc;
+        PBP_CUDA(cudaMemsetAsync(ctx->bctl.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
+        PBP_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    for (int c = 0; c < nchunks; ++c) {
+        const long long off = bounds[c];
+        const long long cnt = bounds[c + 1] - off;
+        if (cnt <= 0) continue;
+        DecodeSlot& sl = ctx->slot[c % kSlots];
+        cudaStream_t st = sl.stream;
+        PBP_CUDA(cudaMemcpyAsync(ctx->llr.p + off * n, llrs + off * n, (size_t)cnt * n * 4, cudaMemcpyHostToDevice, st));
+        DecodeReq r;
+        r.kind = decoder;
+        r.llr = ctx->llr.p + off * n;
+        r.frames = cnt;
+        r.alpha = alpha;
+        r.max_iter = max_iter;
+        r.u_bits = ctx->ubits.p + off * nw;
+        r.iters = ctx->iters.p + off;
+        r.pe = ctx->pe.p + off;
+        r.stop = ctx->stop.p + off;
+        r.nev = ctx->nev.p + off;
+        if (fast) {
+            r.list = ctx->blist.p;
+            r.list_len = ctx->bctl.p;
+            r.frame_base = off;
+        }
+        if ((rc = run_decode(ctx, r, sl, st))) return rc;
+        if (out) {
+            if (out->u_hat_bits)
+                PBP_CUDA(cudaMemcpyAsync(out->u_hat_bits + off * nw, r.u_bits, (size_t)cnt * nw * 4,
+                                         cudaMemcpyDeviceToHost, st));
+            if (out->iterations)
+                PBP_CUDA(cudaMemcpyAsync(out->iterations + off, r.iters, (size_t)cnt * 4, cudaMemcpyDeviceToHost, st));
+            if (out->pe) PBP_CUDA(cudaMemcpyAsync(out->pe + off, r.pe, (size_t)cnt * 8, cudaMemcpyDeviceToHost, st));
+            if (out->stop) PBP_CUDA(cudaMemcpyAsync(out->stop + off, r.stop, (size_t)cnt, cudaMemcpyDeviceToHost, st));
+            if (out->n_events)
+                PBP_CUDA(cudaMemcpyAsync(out->n_events + off, r.nev, (size_t)cnt * 4, cudaMemcpyDeviceToHost, st));
+        }
+    }
+    for (int i = 0; i < kSlots; ++i) PBP_CUDA(cudaStreamSynchronize(ctx->slot[i].stream));
+    if (!fast) return PBP_OK;
+    unsigned long long listed = 0;
+    PBP_CUDA(cudaMemcpy(&listed, ctx->bctl.p, sizeof(listed), cudaMemcpyDeviceToHost));
+    ctx->rerouted_host = (long long)listed;
+    if (listed == 0) return PBP_OK;
+    DecodeReq g;
+    g.kind = decoder;
+    g.llr = ctx->llr.p;
+    g.frames = frames;
+    g.alpha = alpha;
+    g.max_iter = max_iter;
+    g.u_bits = ctx->ubits.p;
+    g.iters = ctx->iters.p;
+    g.pe = ctx->pe.p;
+    g.stop = ctx->stop.p;
+    g.nev = ctx->nev.p;
+    g.list = ctx->blist.p;
+    g.list_len = ctx->bctl.p;
     cudaStream_t st = ctx->stream;
-    if (frames > 0)
-        PBP_CUDA(cudaMemcpyAsync(ctx->llr.p, llrs, (size_t)frames * n * 4, cudaMemcpyHostToDevice, st));
-    DecodeReq r;
-    r.kind = decoder;
-    r.llr = ctx->llr.p;
-    r.frames = frames;
-    r.alpha = alpha;
-    r.max_iter = max_iter;
-    r.u_bits = ctx->ubits.p;
-    r.iters = ctx->iters.p;
-    r.pe = ctx->pe.p;
-    r.stop = ctx->stop.p;
-    r.nev = ctx->nev.p;
-    if ((rc = run_decode(ctx, r, st))) return rc;
-    if (out && frames > 0) {
+    if ((rc = run_generic_list(ctx, g, ctx->slot[0], st, (long long)listed))) return rc;
+    if (out) {  // results again, now with the re-routed frames
         if (out->u_hat_bits)
-            PBP_CUDA(cudaMemcpyAsync(out->u_hat_bits, ctx->ubits.p, (size_t)frames * nw * 4, cudaMemcpyDeviceToHost, st));
+            PBP_CUDA(cudaMemcpyAsync(out->u_hat_bits, g.u_bits, (size_t)frames * nw * 4, cudaMemcpyDeviceToHost, st));
         if (out->iterations)
-            PBP_CUDA(cudaMemcpyAsync(out->iterations, ctx->iters.p, (size_t)frames * 4, cudaMemcpyDeviceToHost, st));
-        if (out->pe) PBP_CUDA(cudaMemcpyAsync(out->pe, ctx->pe.p, (size_t)frames * 8, cudaMemcpyDeviceToHost, st));
-        if (out->stop) PBP_CUDA(cudaMemcpyAsync(out->stop, ctx->stop.p, (size_t)frames, cudaMemcpyDeviceToHost, st));
+            PBP_CUDA(cudaMemcpyAsync(out->iterations, g.iters, (size_t)frames * 4, cudaMemcpyDeviceToHost, st));
+        if (out->pe) PBP_CUDA(cudaMemcpyAsync(out->pe, g.pe, (size_t)frames * 8, cudaMemcpyDeviceToHost, st));
+        if (out->stop) PBP_CUDA(cudaMemcpyAsync(out->stop, g.stop, (size_t)frames, cudaMemcpyDeviceToHost, st));
         if (out->n_events)
-            PBP_CUDA(cudaMemcpyAsync(out->n_events, ctx->nev.p, (size_t)frames * 4, cudaMemcpyDeviceToHost, st));
+            PBP_CUDA(cudaMemcpyAsync(out->n_events, g.nev, (size_t)frames * 4, cudaMemcpyDeviceToHost, st));
     }
     PBP_CUDA(cudaStreamSynchronize(st));
     return PBP_OK;
@@ -499,7 +679,8 @@ int pbp_decode_trace(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
     r.nev = ctx->nev.p;
     r.events = ctx->events.p;
     r.ev_cap = cap;
-    if ((rc = run_decode(ctx, r, st))) return rc;
+    if ((rc = begin_call(ctx, 1))) return rc;
+    if ((rc = run_decode(ctx, r, ctx->slot[0], st))) return rc;
     std::vector<uint32_t> bits(nw);
     int it = 0, sp8 = 0, ne = 0;
     long long act = 0;
@@ -583,7 +764,8 @@ int pbp_decode_count_device(pbp_ctx* ctx, const pbp_code* code, int decoder, con
     r.max_iter = max_iter;
     r.truth = u_dev;
     r.counters = reinterpret_cast<unsigned long long*>(counters_dev);
-    return run_decode(ctx, r, pick(ctx, stream));
+    if ((rc = begin_call(ctx, 1))) return rc;
+    return run_decode(ctx, r, ctx->slot[0], pick(ctx, stream));
 }
 
 int pbp_simulate_point_device(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed,
@@ -599,6 +781,7 @@ int pbp_simulate_point_device(pbp_ctx* ctx, const pbp_code* code, int decoder, u
     const long long chunk = std::max<long long>(1, std::min<long long>(frames, (1ll << 26) / n));
     if ((rc = ctx->llr.ensure((size_t)chunk * n)) || (rc = ctx->truth.ensure((size_t)chunk * nw))) return rc;
     cudaStream_t st = pick(ctx, stream);
+    if ((rc = begin_call(ctx, (int)((frames + chunk - 1) / chunk)))) return rc;
     for (long long done = 0; done < frames; done += chunk) {
         const long long c = std::min(chunk, frames - done);
         if ((rc = run_generate(ctx, seed, first_trial + done, c, ebn0_db, noiseless, ctx->llr.p, nullptr,
@@ -612,7 +795,7 @@ int pbp_simulate_point_device(pbp_ctx* ctx, const pbp_code* code, int decoder, u
         r.max_iter = max_iter;
         r.truth = ctx->truth.p;
         r.counters = reinterpret_cast<unsigned long long*>(counters_dev);
-        if ((rc = run_decode(ctx, r, st))) return rc;
+        if ((rc = run_decode(ctx, r, ctx->slot[0], st))) return rc;
     }
     return PBP_OK;
 }

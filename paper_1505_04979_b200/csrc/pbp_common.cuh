@@ -44,8 +44,9 @@ struct DecodeArgs {
     unsigned long long* queue;        // atomic frame counter (zeroed before launch)
     // re-route list: the fast kernel appends frames it cannot take; the
     // generic kernel consumes it when list_mode != 0.
-    long long* list;
+    long long* list;                  // frame indices + frame_base
     unsigned long long* list_len;
+    long long frame_base;             // index of this launch's frame 0 in the list's numbering
     int list_mode;
     float* r0s;                       // warp kernel: per-CTA channel LLRs (n floats each)
     float* scratch;                   // generic kernel: per-CTA message arrays

@@ -122,6 +122,26 @@ def test_clamp_and_nonfinite_frames_rerouted(ctx, n):
             assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), (kind, f)
 
 
+def test_chunked_batch_matches_single_launches(ctx):
+    """pbp_decode_batch pipelines large batches over several streams (chunks of
+    >= 16384 frames); results and the re-route count equal one launch per part."""
+    n, frames = 256, 70_000
+    code = P.PolarCode.construct(n, n // 2, Z0)
+    llr, _, _ = P.generate(code, 9, 0, frames, 2.0, ctx=ctx)
+    big = [5, 16_400, 33_000, 52_001, 69_999]          # re-routed frames in several chunks
+    llr[big, 7] = 1e30
+    for kind in ("gmatrix", "csfg"):
+        whole = P.decode_batch(code, kind, llr, 0.9375, 30, ctx=ctx)
+        launches, rerouted = ctx.last_launch_info()
+        assert rerouted == len(big) and launches >= 3, (launches, rerouted)
+        for a, b in ((0, 16_000), (16_000, 30_000), (30_000, frames)):
+            part = P.decode_batch(code, kind, llr[a:b], 0.9375, 30, ctx=ctx)
+            for f in whole:
+                assert np.array_equal(whole[f][a:b], part[f]), (kind, f, a)
+    exp = O.decode_batch("csfg", code.frozen, llr[big], 0.9375, 30, prec=32)
+    assert np.array_equal(P.unpack_bits(whole["u_hat_bits"][big], n), exp["u_hat"])
+
+
 @pytest.mark.parametrize("n,seed,ebn0", [(64, 4242, 2.0), (1024, 2, 3.0), (256, 5, 2.5), (4096, 4, 2.5)])
 def test_channel_generation_matches_reference_stream(ctx, n, seed, ebn0):
     fz = O.construct(n, n // 2, Z0 if n != 64 else 0.5)
