@@ -150,6 +150,21 @@ def cpu_reference_run(seconds_per_step=8.0, steps=1, warmup=0, want_threads=None
                       f"of config 2, fp64 reference decode_csfg, {threads} threads, LLRs pre-generated"}
 
 
+def dram_traffic(frames_per_launch):
+    """DRAM bytes (read + write) per decode launch, from the committed ncu capture
+    (profiles/*_ncu_summary.json: dram__bytes_read.sum + dram__bytes_write.sum of
+    bp_warp_kernel<10,2>, scaled per frame to this launch size); None if absent."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")))
+    if not files:
+        return None
+    try:
+        s = json.load(open(files[-1]))
+        return float(s["csfg"]["dram_bytes_per_frame"]) * frames_per_launch
+    except Exception:
+        return None
+
+
 def cpu_model():
     try:
         for ln in open("/proc/cpuinfo"):
@@ -309,7 +324,7 @@ def main():
             "fer_per_point": [float(t[2] / max(t[0], 1)) for t in tot],
             "gpu_launches": steps * len(SNRS) * 2,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "TOP/s (fp32 ops)",
-                         "frac": achieved / peak_tops, "traffic": None,
+                         "frac": achieved / peak_tops, "traffic": dram_traffic(frames),
                          "note": f"9 fp32 ops per PE activation (reference pe_activations counter); peak = "
                                  f"{sm_count} SMs x 128 lanes x {fclk / 1e6:.0f} MHz (sm_max_mhz of "
                                  "MEASURED_PEAKS.json); achieved from CUDA-event launch times"},
