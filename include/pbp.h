@@ -15,7 +15,8 @@
  *   - Decoders compute in fp32 in the reference's fp32 operation order
  *     (SURVEY.md 8c "ref32"): hard decisions, iteration counts, PE counts,
  *     stop reasons and freeze-event counts equal the reference compiled in
- *     fp32 on the same fp32 LLRs.
+ *     fp32 on the same fp32 LLRs. The *_f64 entry points decode double LLRs
+ *     in the reference's own (shipped) double arithmetic instead ("ref64").
  *   - Every call returns PBP_OK (0) or a status; pbp_last_error() gives the
  *     message (thread-local). The reference throws std::invalid_argument /
  *     std::runtime_error with the same texts; the C++ wrapper rethrows them.
@@ -126,6 +127,25 @@ int pbp_decode_trace(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
                      float alpha, int32_t max_iter, uint8_t* u_hat, int32_t* iterations,
                      int64_t* pe, int32_t* stop, int32_t* n_events, int32_t* events,
                      int32_t events_cap);
+
+/* ---- fp64: the reference as shipped --------------------------------------
+ * Same calls with double LLRs and alpha, decoded in double in the reference's
+ * operation order (src/bp_core.cpp:13-137 with `double`): results equal the
+ * shipped fp64 reference frame by frame, converged or not. Served by the
+ * generic kernel (about an order of magnitude below the fp32 fast path). */
+int pbp_decode_batch_f64(pbp_ctx* ctx, const pbp_code* code, int decoder, const double* llrs,
+                         int64_t frames, double alpha, int32_t max_iter, pbp_frame_out* out);
+int pbp_decode_batch_f64_device(pbp_ctx* ctx, const pbp_code* code, int decoder,
+                                const double* llrs_dev, int64_t frames, double alpha,
+                                int32_t max_iter, pbp_frame_out* out_dev, void* stream);
+int pbp_decode_trace_f64(pbp_ctx* ctx, const pbp_code* code, int decoder, const double* llrs,
+                         double alpha, int32_t max_iter, uint8_t* u_hat, int32_t* iterations,
+                         int64_t* pe, int32_t* stop, int32_t* n_events, int32_t* events,
+                         int32_t events_cap);
+/* run_point's counters with the reference's double LLRs (src/sim_harness.cpp:67-73). */
+int pbp_simulate_point_f64(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed,
+                           int64_t first_trial, int64_t frames, double ebn0_db, int noiseless,
+                           double alpha, int32_t max_iter, pbp_counters* out);
 
 /* ---- channel -----------------------------------------------------------
  * decode_trial's frame generation (src/sim_harness.cpp:67-73): per trial

@@ -39,5 +39,10 @@ std::vector<double> transmit_awgn(std::span<const double> symbols, const Channel
 void generate_frames(const PolarCode& code, std::uint64_t seed, std::int64_t first_trial,
                      std::int64_t count, const ChannelConfig& config, std::vector<float>& llrs,
                      std::vector<Bits>* u_words = nullptr);
+// The same frames with the fp64 LLRs (the CUDA log/cos may differ from glibc's
+// in the last bits near y = 0; the fp32 LLRs above match the host exactly).
+void generate_frames(const PolarCode& code, std::uint64_t seed, std::int64_t first_trial,
+                     std::int64_t count, const ChannelConfig& config, std::vector<double>& llrs,
+                     std::vector<Bits>* u_words = nullptr);
 
 }  // namespace polarbp

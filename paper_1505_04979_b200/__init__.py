@@ -267,13 +267,16 @@ def pack_bits(bits: np.ndarray) -> np.ndarray:
 
 
 def decode_batch(code: PolarCode, decoder, llrs, alpha: float = 0.9375, max_iter: int = 40,
-                 ctx: Optional[Context] = None):
-    """Batched decode of frames x n fp32 LLRs (host arrays) through pbp_decode_batch.
+                 ctx: Optional[Context] = None, precision: str = "f32"):
+    """Batched decode of frames x n LLRs (host arrays) through pbp_decode_batch
+    (precision "f32": fp32 in the reference's operation order, the fast path) or
+    pbp_decode_batch_f64 ("f64": double, the reference as shipped).
 
     Returns dict: u_hat_bits (frames, ceil(n/32)) uint32, iterations, pe, stop, n_events.
     """
     ctx = ctx or default_context()
-    llr = np.ascontiguousarray(np.asarray(llrs, dtype=np.float32))
+    f64 = _precision(precision)
+    llr = np.ascontiguousarray(np.asarray(llrs, dtype=np.float64 if f64 else np.float32))
     if llr.ndim == 1:
         llr = llr.reshape(1, -1)
     if llr.shape[1] != code.n:
@@ -290,14 +293,25 @@ def decode_batch(code: PolarCode, decoder, llrs, alpha: float = 0.9375, max_iter
     fo = _abi.PbpFrameOut(_abi.u32p(out["u_hat_bits"]), _abi.i32p(out["iterations"]),
                           _abi.i64p(out["pe"]), _abi.u8p(out["stop"]), _abi.i32p(out["n_events"]))
     cs = code.c_struct()
-    _check(lib.pbp_decode_batch(ctx.handle, C.byref(cs), _kind(decoder), _abi.f32p(llr), frames,
-                                float(alpha), int(max_iter), C.byref(fo)))
+    if f64:
+        _check(lib.pbp_decode_batch_f64(ctx.handle, C.byref(cs), _kind(decoder), _abi.f64p(llr), frames,
+                                        float(alpha), int(max_iter), C.byref(fo)))
+    else:
+        _check(lib.pbp_decode_batch(ctx.handle, C.byref(cs), _kind(decoder), _abi.f32p(llr), frames,
+                                    float(alpha), int(max_iter), C.byref(fo)))
     return out
 
 
-def _decode_one(code: PolarCode, kind: int, llrs, alpha, max_iter, events=None, ctx=None):
+def _precision(p: str) -> bool:
+    if p not in ("f32", "f64"):
+        raise ValueError(f"precision must be 'f32' or 'f64', got {p!r}")
+    return p == "f64"
+
+
+def _decode_one(code: PolarCode, kind: int, llrs, alpha, max_iter, events=None, ctx=None, precision="f32"):
     ctx = ctx or default_context()
-    llr = np.ascontiguousarray(np.asarray(llrs, dtype=np.float32).reshape(-1))
+    f64 = _precision(precision)
+    llr = np.ascontiguousarray(np.asarray(llrs, dtype=np.float64 if f64 else np.float32).reshape(-1))
     if llr.size != code.n:
         raise ValueError("init_state: LLR length != n")
     cap = 4096
@@ -306,9 +320,9 @@ def _decode_one(code: PolarCode, kind: int, llrs, alpha, max_iter, events=None, 
     it, sp, ne = C.c_int32(), C.c_int32(), C.c_int32()
     pe = C.c_int64()
     cs = code.c_struct()
-    _check(lib.pbp_decode_trace(ctx.handle, C.byref(cs), kind, _abi.f32p(llr), float(alpha),
-                                int(max_iter), _abi.u8p(u), C.byref(it), C.byref(pe), C.byref(sp),
-                                C.byref(ne), _abi.i32p(ev), cap))
+    fn, lp = (lib.pbp_decode_trace_f64, _abi.f64p(llr)) if f64 else (lib.pbp_decode_trace, _abi.f32p(llr))
+    _check(fn(ctx.handle, C.byref(cs), kind, lp, float(alpha), int(max_iter), _abi.u8p(u), C.byref(it),
+              C.byref(pe), C.byref(sp), C.byref(ne), _abi.i32p(ev), cap))
     if events is not None:
         events.clear()
         for i in range(min(ne.value, cap)):
@@ -316,20 +330,22 @@ def _decode_one(code: PolarCode, kind: int, llrs, alpha, max_iter, events=None, 
     return DecodeOutcome(u, extract_info_bits(code, u), it.value, pe.value, sp.value, ne.value)
 
 
-def decode_baseline(code: PolarCode, llrs, alpha: float, max_iter: int, ctx=None) -> DecodeOutcome:
+def decode_baseline(code: PolarCode, llrs, alpha: float, max_iter: int, ctx=None,
+                    precision: str = "f32") -> DecodeOutcome:
     """decode_baseline (bp_core.hpp:84) on the GPU."""
-    return _decode_one(code, 0, llrs, alpha, max_iter, ctx=ctx)
+    return _decode_one(code, 0, llrs, alpha, max_iter, ctx=ctx, precision=precision)
 
 
-def decode_gmatrix(code: PolarCode, llrs, alpha: float, max_iter: int, ctx=None) -> DecodeOutcome:
+def decode_gmatrix(code: PolarCode, llrs, alpha: float, max_iter: int, ctx=None,
+                   precision: str = "f32") -> DecodeOutcome:
     """decode_gmatrix (bp_core.hpp:86) on the GPU."""
-    return _decode_one(code, 1, llrs, alpha, max_iter, ctx=ctx)
+    return _decode_one(code, 1, llrs, alpha, max_iter, ctx=ctx, precision=precision)
 
 
 def decode_csfg(code: PolarCode, llrs, alpha: float, max_iter: int,
-                events: Optional[list] = None, ctx=None) -> DecodeOutcome:
+                events: Optional[list] = None, ctx=None, precision: str = "f32") -> DecodeOutcome:
     """decode_csfg (csfg_freeze.hpp:109-111) on the GPU; `events` receives FreezeEvents."""
-    return _decode_one(code, 2, llrs, alpha, max_iter, events=events, ctx=ctx)
+    return _decode_one(code, 2, llrs, alpha, max_iter, events=events, ctx=ctx, precision=precision)
 
 
 # ---------------------------------------------------------------- channel / Monte Carlo
@@ -357,14 +373,15 @@ COUNTER_FIELDS = ("frames", "bit_errors", "frame_errors", "sum_iters", "sum_iter
 
 def simulate_point(code: PolarCode, decoder, seed: int, first_trial: int, frames: int,
                    ebn0_db: float, alpha: float = 0.9375, max_iter: int = 40,
-                   noiseless: bool = False, ctx=None) -> dict:
-    """Counters (Accumulator, sim_harness.cpp:56-63) over trials [first, first+frames)."""
+                   noiseless: bool = False, ctx=None, precision: str = "f32") -> dict:
+    """Counters (Accumulator, sim_harness.cpp:56-63) over trials [first, first+frames);
+    precision "f64" decodes the reference's double LLRs in double (as shipped)."""
     ctx = ctx or default_context()
     c = _abi.PbpCounters()
     cs = code.c_struct()
-    _check(lib.pbp_simulate_point(ctx.handle, C.byref(cs), _kind(decoder), C.c_uint64(seed),
-                                  int(first_trial), int(frames), float(ebn0_db),
-                                  int(bool(noiseless)), float(alpha), int(max_iter), C.byref(c)))
+    fn = lib.pbp_simulate_point_f64 if _precision(precision) else lib.pbp_simulate_point
+    _check(fn(ctx.handle, C.byref(cs), _kind(decoder), C.c_uint64(seed), int(first_trial), int(frames),
+              float(ebn0_db), int(bool(noiseless)), float(alpha), int(max_iter), C.byref(c)))
     vals = [c.frames, c.bit_errors, c.frame_errors, c.sum_iters, c.sum_iters_sq, c.sum_pe,
             c.sum_events, c.stop_hist[0], c.stop_hist[1], c.stop_hist[2]]
     return dict(zip(COUNTER_FIELDS, [int(v) for v in vals]))
@@ -384,6 +401,7 @@ class SimConfig:
     seed: int = 1
     workers: int = 1
     noiseless: bool = False
+    precision: str = "f32"   # B200 addition: "f64" decodes in double, as shipped
 
 
 @dataclass
@@ -450,7 +468,7 @@ def run_point(cfg: SimConfig, snr_db: float, ctx=None) -> List[PointStats]:
             batch = min(K_BATCH, cfg.max_frames - frames)
             for d, kind in enumerate(cfg.decoders):
                 c = simulate_point(cfg.code, kind, cfg.seed, frames, batch, snr_db, cfg.alpha,
-                                   cfg.max_iter, cfg.noiseless, ctx)
+                                   cfg.max_iter, cfg.noiseless, ctx, precision=cfg.precision)
                 for key in COUNTER_FIELDS:
                     accs[d][key] += c[key]
             frames += batch

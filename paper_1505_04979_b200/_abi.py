@@ -65,6 +65,16 @@ SIGNATURES = {
                                    C.POINTER(C.c_uint8), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                    C.c_int32]),
+    "pbp_decode_batch_f64": (C.c_int, [_P, _CP, C.c_int, C.POINTER(C.c_double), C.c_int64, C.c_double,
+                                       C.c_int32, C.POINTER(PbpFrameOut)]),
+    "pbp_decode_batch_f64_device": (C.c_int, [_P, _CP, C.c_int, C.POINTER(C.c_double), C.c_int64,
+                                              C.c_double, C.c_int32, C.POINTER(PbpFrameOut), _P]),
+    "pbp_decode_trace_f64": (C.c_int, [_P, _CP, C.c_int, C.POINTER(C.c_double), C.c_double, C.c_int32,
+                                       C.POINTER(C.c_uint8), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                       C.c_int32]),
+    "pbp_simulate_point_f64": (C.c_int, [_P, _CP, C.c_int, C.c_uint64, C.c_int64, C.c_int64, C.c_double,
+                                         C.c_int, C.c_double, C.c_int32, C.POINTER(PbpCounters)]),
     "pbp_generate_device": (C.c_int, [_P, _CP, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_int,
                                       C.POINTER(C.c_float), C.POINTER(C.c_double),
                                       C.POINTER(C.c_uint32), _P]),

@@ -12,22 +12,41 @@
 //
 // Roles: (1) the decode path for n outside the warp-resident kernel's range
 // (n < 128 and n >= 2048), (2) the path for frames the fast kernel
-// re-routes (|LLR| > kClampFreeBound or non-finite).
+// re-routes (|LLR| > kClampFreeBound or non-finite), (3) instantiated on
+// double, the reference as shipped (its fp64 operation order; DecodeArgs
+// llr64 / alpha64).
 #include "pbp_common.cuh"
 
 namespace pbp {
 
 namespace {
 
-__device__ __forceinline__ float ref_sgn(float v) { return v < 0.f ? -1.f : 1.f; }
-__device__ __forceinline__ float ref_min(float a, float b) { return b < a ? b : a; }
-__device__ __forceinline__ float ref_clamp(float v) {
-    return v < -kCap ? -kCap : (kCap < v ? kCap : v);
+// The reference's arithmetic (src/bp_core.cpp:13-32) for T = float (its
+// fp32 operation order) and T = double (as shipped); every product and sum
+// rounded on its own (-fmad=false and explicit _rn intrinsics).
+template <typename T> struct RealOps;
+template <> struct RealOps<float> {
+    static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+    static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+    static __device__ __forceinline__ float abs(float a) { return fabsf(a); }
+    static constexpr float cap = kCap;
+};
+template <> struct RealOps<double> {
+    static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+    static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+    static __device__ __forceinline__ double abs(double a) { return fabs(a); }
+    static constexpr double cap = 1e30;  // LLR_CAP (include/polarbp/bp_core.hpp:21)
+};
+template <typename T> __device__ __forceinline__ T ref_sgn(T v) { return v < T(0) ? T(-1) : T(1); }
+template <typename T> __device__ __forceinline__ T ref_min(T a, T b) { return b < a ? b : a; }
+template <typename T> __device__ __forceinline__ T ref_clamp(T v) {
+    const T c = RealOps<T>::cap;
+    return v < -c ? -c : (c < v ? c : v);
 }
 // alpha * sgn(a) * sgn(b) * min(|a|, |b|), left to right, no contraction
-__device__ __forceinline__ float ref_f(float alpha, float a, float b) {
-    return __fmul_rn(__fmul_rn(__fmul_rn(alpha, ref_sgn(a)), ref_sgn(b)),
-                     ref_min(fabsf(a), fabsf(b)));
+template <typename T> __device__ __forceinline__ T ref_f(T alpha, T a, T b) {
+    using O = RealOps<T>;
+    return O::mul(O::mul(O::mul(alpha, ref_sgn(a)), ref_sgn(b)), ref_min(O::abs(a), O::abs(b)));
 }
 
 // Polar transform of `nbits` bits held in words[0..ceil(nbits/32)) of
@@ -48,8 +67,10 @@ __device__ void cta_transform(uint32_t* words, int nbits) {
 
 }  // namespace
 
-template <int BLOCK>
+template <int BLOCK, typename T>
 __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
+    using O = RealOps<T>;
+    const T cap = O::cap;
     extern __shared__ uint32_t smem[];
     const int n = a.n, m = a.m;
     const int nw_all = (n + 31) >> 5;
@@ -65,10 +86,11 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    float* L = a.scratch + (long long)blockIdx.x * a.scratch_stride;  // (m+1) x n
-    float* R0 = L + (size_t)(m + 1) * n;
-    float* R = R0 + n;
-    const float* Rm = (m == 0) ? R0 : R;
+    T* L = reinterpret_cast<T*>(a.scratch) + (long long)blockIdx.x * a.scratch_stride;  // (m+1) x n
+    T* R0 = L + (size_t)(m + 1) * n;
+    T* R = R0 + n;
+    const T* Rm = (m == 0) ? R0 : R;
+    const T alpha = sizeof(T) == 8 ? T(a.alpha64) : T(a.alpha);
     const bool csfg = a.kind == 2;
 
     for (;;) {
@@ -91,11 +113,11 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
         if (frame < 0) break;
 
         // init_state (src/bp_core.cpp:43-56)
-        const float* llr = a.llr + frame * (long long)n;
         for (int r = tid; r < n; r += BLOCK) {
-            R0[r] = ref_clamp(llr[r]);
-            for (int s = 0; s < m; ++s) L[(size_t)s * n + r] = 0.f;
-            L[(size_t)m * n + r] = a.frozen_rows[r] ? kCap : 0.f;
+            const T v = sizeof(T) == 8 ? T(a.llr64[frame * (long long)n + r]) : T(a.llr[frame * (long long)n + r]);
+            R0[r] = ref_clamp(v);
+            for (int s = 0; s < m; ++s) L[(size_t)s * n + r] = T(0);
+            L[(size_t)m * n + r] = a.frozen_rows[r] ? cap : T(0);
             fst[r] = kNotFrozen;
         }
         for (int q = tid; q < nw_all; q += BLOCK) dec_u[q] = 0u;
@@ -114,19 +136,19 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
                 // ---- stage_pass (src/bp_core.cpp:58-80) ----
                 const int ld = m - 1 - s;
                 const int d = 1 << ld;
-                const float* Rin = (s == 0) ? R0 : R;
-                float* Ls = L + (size_t)s * n;
-                const float* Ls1 = L + (size_t)(s + 1) * n;
+                const T* Rin = (s == 0) ? R0 : R;
+                T* Ls = L + (size_t)s * n;
+                const T* Ls1 = L + (size_t)(s + 1) * n;
                 for (int p = tid; p < n / 2; p += BLOCK) {
                     const int r = ((p >> ld) << (ld + 1)) | (p & (d - 1));
                     if (csfg && (int)fst[r] < s) continue;  // is_pe_active (csfg_freeze.cpp:95-97)
-                    const float lt = Ls1[r], lb = Ls1[r + d], rt = Rin[r], rb = Rin[r + d];
-                    const float cross = ref_f(a.alpha, lt, rt);
-                    const float sum_bot = __fadd_rn(lb, rb);
-                    Ls[r] = ref_clamp(ref_f(a.alpha, lt, sum_bot));
-                    Ls[r + d] = ref_clamp(__fadd_rn(lb, cross));
-                    R[r] = ref_clamp(ref_f(a.alpha, rt, sum_bot));
-                    R[r + d] = ref_clamp(__fadd_rn(rb, cross));
+                    const T lt = Ls1[r], lb = Ls1[r + d], rt = Rin[r], rb = Rin[r + d];
+                    const T cross = ref_f(alpha, lt, rt);
+                    const T sum_bot = O::add(lb, rb);
+                    Ls[r] = ref_clamp(ref_f(alpha, lt, sum_bot));
+                    Ls[r + d] = ref_clamp(O::add(lb, cross));
+                    R[r] = ref_clamp(ref_f(alpha, rt, sum_bot));
+                    R[r + d] = ref_clamp(O::add(rb, cross));
                     ++act;
                 }
                 __syncthreads();
@@ -140,7 +162,7 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
                 const int start = index * sz;
                 const int nw = (sz + 31) >> 5;
                 for (int i = tid; i < nw * 32; i += BLOCK) {
-                    const bool b = (i < sz) && (R[start + i] < 0.f);
+                    const bool b = (i < sz) && (R[start + i] < T(0));
                     const uint32_t w = __ballot_sync(0xffffffffu, b);
                     if (lane == 0) wb0[i >> 5] = w;
                 }
@@ -158,7 +180,7 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
                 if (accept) {
                     for (int i = tid; i < sz; i += BLOCK) {
                         const int r = start + i;
-                        L[(size_t)(s + 1) * n + r] = (R[r] < 0.f) ? -kCap : kCap;
+                        L[(size_t)(s + 1) * n + r] = (R[r] < T(0)) ? -cap : cap;
                         if ((int)fst[r] > s) fst[r] = (uint8_t)s;
                     }
                     if (sz >= 32) {
@@ -193,8 +215,8 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
                 bool ub = false, xb = false;
                 if (i < n) {
                     ub = (i < pin) ? ((dec_u[i >> 5] >> (i & 31)) & 1u)
-                                   : (!a.frozen_rows[i] && Rm[i] < 0.f);
-                    xb = __fadd_rn(R0[i], L[i]) < 0.f;
+                                   : (!a.frozen_rows[i] && Rm[i] < T(0));
+                    xb = O::add(R0[i], L[i]) < T(0);
                 }
                 const uint32_t wu = __ballot_sync(0xffffffffu, ub);
                 const uint32_t wx = __ballot_sync(0xffffffffu, xb);
@@ -226,7 +248,7 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
             bool ub = false;
             if (i < n)
                 ub = (i < pin) ? ((dec_u[i >> 5] >> (i & 31)) & 1u)
-                               : (!a.frozen_rows[i] && Rm[i] < 0.f);
+                               : (!a.frozen_rows[i] && Rm[i] < T(0));
             const uint32_t w = __ballot_sync(0xffffffffu, ub);
             if (lane == 0) {
                 if (a.u_bits) a.u_bits[frame * nw_all + (i >> 5)] = w;
@@ -267,21 +289,27 @@ size_t generic_smem_bytes(int n) {
     return (size_t)3 * nw * 4 + (size_t)n + 16;
 }
 
-long long generic_scratch_floats(int n, int m) {
+// per-CTA message scratch in elements of the decode precision (float or
+// double); scratch_stride is in those elements
+long long generic_scratch_elems(int n, int m) {
     long long f = (long long)(m + 3) * n;
     return (f + 63) / 64 * 64;
 }
 
-cudaError_t launch_generic(const DecodeArgs& a, int grid, cudaStream_t stream) {
+template <typename T>
+static cudaError_t launch_t(const DecodeArgs& a, int grid, cudaStream_t stream) {
     const size_t smem = generic_smem_bytes(a.n);
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(bp_generic_kernel<kGenericBlock>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(bp_generic_kernel<kGenericBlock, T>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    bp_generic_kernel<kGenericBlock><<<grid, kGenericBlock, smem, stream>>>(a);
+    bp_generic_kernel<kGenericBlock, T><<<grid, kGenericBlock, smem, stream>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_generic(const DecodeArgs& a, int grid, cudaStream_t stream) {
+    return a.llr64 ? launch_t<double>(a, grid, stream) : launch_t<float>(a, grid, stream);
 }
 
 }  // namespace pbp

@@ -18,7 +18,7 @@ namespace pbp {
 // kernels (bp_generic.cu, bp_warp.cu, channel.cu)
 cudaError_t launch_generic(const DecodeArgs& a, int grid, cudaStream_t stream);
 size_t generic_smem_bytes(int n);
-long long generic_scratch_floats(int n, int m);
+long long generic_scratch_elems(int n, int m);
 cudaError_t launch_warp(const DecodeArgs& a, int grid, cudaStream_t st);
 int warp_kernel_supported(int m);
 int warp_blocks_per_sm(int m, int kind);
@@ -107,6 +107,7 @@ struct pbp_ctx {
     DevBuf<unsigned long long> bctl;      // [0] its length, [1] generic queue
     // host-API staging
     DevBuf<float> llr;
+    DevBuf<double> llr64;
     DevBuf<uint32_t> ubits, truth;
     DevBuf<int> iters, nev, events;
     DevBuf<long long> pe;
@@ -161,6 +162,8 @@ int upload_code(pbp_ctx* ctx, const pbp_code* code) {
 struct DecodeReq {
     int kind = 0;
     const float* llr = nullptr;
+    const double* llr64 = nullptr;  // set: decode in fp64 (the reference as shipped)
+    double alpha64 = 0.9375;
     long long frames = 0;
     float alpha = 0.9375f;
     int max_iter = 40;
@@ -192,9 +195,9 @@ int begin_call(pbp_ctx* ctx, int max_sets) {
 // Grid of the generic kernel: every frame when it decodes alone, the
 // re-routed frames (at most one per SM at a time) after the warp kernel;
 // bounded by 1 GiB of per-CTA scratch.
-long long generic_grid(const pbp_ctx* ctx, long long frames, bool fast) {
+long long generic_grid(const pbp_ctx* ctx, long long frames, bool fast, int esz = 1) {
     const long long gfm = fast ? std::min<long long>(frames, ctx->sm_count) : frames;
-    const long long stride = pbp::generic_scratch_floats(ctx->n, ctx->m);
+    const long long stride = pbp::generic_scratch_elems(ctx->n, ctx->m) * esz;
     long long grid = std::min<long long>(gfm, (long long)ctx->sm_count * 4);
     const long long max_scratch_floats = 1ll << 28;  // 1 GiB
     return std::max<long long>(1, std::min<long long>(grid, max_scratch_floats / stride));
@@ -211,7 +214,7 @@ int size_slot(pbp_ctx* ctx, DecodeSlot& s, int kind, long long frames) {
         if ((rc = s.r0s.ensure((size_t)(grid * ctx->n)))) return rc;
     }
     const bool fast = !ctx->force_generic && pbp::warp_kernel_supported(ctx->m);
-    return s.scratch.ensure((size_t)generic_grid(ctx, frames, fast) * pbp::generic_scratch_floats(ctx->n, ctx->m));
+    return s.scratch.ensure((size_t)generic_grid(ctx, frames, fast) * pbp::generic_scratch_elems(ctx->n, ctx->m));
 }
 
 // Launch the decode of `frames` frames already on the device, with slot s's
@@ -232,6 +235,8 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
     a.frozen_bits = ctx->frozen_bits.p;
     a.frozen_rows = ctx->frozen_rows.p;
     a.llr = r.llr;
+    a.llr64 = r.llr64;
+    a.alpha64 = r.alpha64;
     a.frames = r.frames;
     a.u_bits = r.u_bits;
     a.iters = r.iters;
@@ -244,7 +249,8 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
     a.counters = r.counters;
     a.list_len = s.ctl.p + 2;
 
-    const bool fast = !r.force_generic && !ctx->force_generic && pbp::warp_kernel_supported(ctx->m);
+    // the warp kernel is fp32 only; fp64 decodes run the generic kernel on double
+    const bool fast = !r.llr64 && !r.force_generic && !ctx->force_generic && pbp::warp_kernel_supported(ctx->m);
     if (fast) {
         a.list = r.list ? r.list : s.list.p;
         if (r.list_len) a.list_len = r.list_len;
@@ -265,10 +271,11 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
         a.list_mode = 0;
     }
     a.queue = s.ctl.p + 1;
-    // generic kernel: bounded grid, per-CTA scratch
-    const long long stride = pbp::generic_scratch_floats(ctx->n, ctx->m);
-    const long long grid = generic_grid(ctx, r.frames, fast);
-    if ((rc = s.scratch.ensure((size_t)(grid * stride)))) return rc;
+    // generic kernel: bounded grid, per-CTA scratch (elements of the decode precision)
+    const int esz = r.llr64 ? 2 : 1;  // in floats
+    const long long stride = pbp::generic_scratch_elems(ctx->n, ctx->m);
+    const long long grid = generic_grid(ctx, r.frames, fast, esz);
+    if ((rc = s.scratch.ensure((size_t)(grid * stride * esz)))) return rc;
     a.scratch = s.scratch.p;
     a.scratch_stride = stride;
     cudaError_t e = pbp::launch_generic(a, (int)grid, st);
@@ -311,7 +318,7 @@ int run_generic_list(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream
     a.list_len = r.list_len;
     a.list_mode = 1;
     a.queue = s.ctl.p + 1;
-    const long long stride = pbp::generic_scratch_floats(ctx->n, ctx->m);
+    const long long stride = pbp::generic_scratch_elems(ctx->n, ctx->m);
     const long long grid = generic_grid(ctx, std::max<long long>(1, listed), false);
     if ((rc = s.scratch.ensure((size_t)(grid * stride)))) return rc;
     a.scratch = s.scratch.p;
@@ -409,6 +416,7 @@ int pbp_ctx_destroy(pbp_ctx* ctx) {
     ctx->rerouted.release();
     ctx->blist.release();
     ctx->bctl.release();
+    ctx->llr64.release();
     ctx->counters.release();
     ctx->llr.release();
     ctx->ubits.release();
@@ -651,9 +659,13 @@ int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
     return PBP_OK;
 }
 
-int pbp_decode_trace(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs, float alpha,
-                     int32_t max_iter, uint8_t* u_hat, int32_t* iterations, int64_t* pe, int32_t* stop,
-                     int32_t* n_events, int32_t* events, int32_t events_cap) {
+}  // extern "C"
+
+namespace {
+// decode_csfg(..., events) for one frame; fp32 (llrs) or fp64 (llrs64)
+int decode_trace_impl(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs, const double* llrs64,
+                      double alpha, int32_t max_iter, uint8_t* u_hat, int32_t* iterations, int64_t* pe,
+                      int32_t* stop, int32_t* n_events, int32_t* events, int32_t events_cap) {
     if (!ctx) return fail(PBP_EINVAL, "null context");
     PBP_CUDA(cudaSetDevice(ctx->device));
     int rc = upload_code(ctx, code);
@@ -665,12 +677,19 @@ int pbp_decode_trace(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
         (rc = ctx->events.ensure((size_t)cap * 5)))
         return rc;
     cudaStream_t st = ctx->stream;
-    PBP_CUDA(cudaMemcpyAsync(ctx->llr.p, llrs, (size_t)n * 4, cudaMemcpyHostToDevice, st));
     DecodeReq r;
+    if (llrs64) {
+        if ((rc = ctx->llr64.ensure(n))) return rc;
+        PBP_CUDA(cudaMemcpyAsync(ctx->llr64.p, llrs64, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+        r.llr64 = ctx->llr64.p;
+        r.alpha64 = alpha;
+    } else {
+        PBP_CUDA(cudaMemcpyAsync(ctx->llr.p, llrs, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+        r.llr = ctx->llr.p;
+        r.alpha = (float)alpha;
+    }
     r.kind = decoder;
-    r.llr = ctx->llr.p;
     r.frames = 1;
-    r.alpha = alpha;
     r.max_iter = max_iter;
     r.u_bits = ctx->ubits.p;
     r.iters = ctx->iters.p;
@@ -702,6 +721,90 @@ int pbp_decode_trace(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
     if (n_events) *n_events = ne;
     if (events && events_cap > 0)
         std::memcpy(events, ev.data(), (size_t)std::min(ne, events_cap) * 5 * 4);
+    return PBP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int pbp_decode_trace(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs, float alpha,
+                     int32_t max_iter, uint8_t* u_hat, int32_t* iterations, int64_t* pe, int32_t* stop,
+                     int32_t* n_events, int32_t* events, int32_t events_cap) {
+    return decode_trace_impl(ctx, code, decoder, llrs, nullptr, alpha, max_iter, u_hat, iterations, pe, stop,
+                             n_events, events, events_cap);
+}
+
+int pbp_decode_trace_f64(pbp_ctx* ctx, const pbp_code* code, int decoder, const double* llrs, double alpha,
+                         int32_t max_iter, uint8_t* u_hat, int32_t* iterations, int64_t* pe, int32_t* stop,
+                         int32_t* n_events, int32_t* events, int32_t events_cap) {
+    if (!llrs) return fail(PBP_EINVAL, "null llrs");
+    return decode_trace_impl(ctx, code, decoder, nullptr, llrs, alpha, max_iter, u_hat, iterations, pe, stop,
+                             n_events, events, events_cap);
+}
+
+int pbp_decode_batch_f64_device(pbp_ctx* ctx, const pbp_code* code, int decoder, const double* llrs_dev,
+                                int64_t frames, double alpha, int32_t max_iter, pbp_frame_out* out_dev,
+                                void* stream) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    PBP_CUDA(cudaSetDevice(ctx->device));
+    int rc = upload_code(ctx, code);
+    if (rc) return rc;
+    DecodeReq r;
+    r.kind = decoder;
+    r.llr64 = llrs_dev;
+    r.alpha64 = alpha;
+    r.frames = frames;
+    r.max_iter = max_iter;
+    if (out_dev) {
+        r.u_bits = out_dev->u_hat_bits;
+        r.iters = out_dev->iterations;
+        r.pe = reinterpret_cast<long long*>(out_dev->pe);
+        r.stop = out_dev->stop;
+        r.nev = out_dev->n_events;
+    }
+    if ((rc = begin_call(ctx, 1))) return rc;
+    return run_decode(ctx, r, ctx->slot[0], pick(ctx, stream));
+}
+
+int pbp_decode_batch_f64(pbp_ctx* ctx, const pbp_code* code, int decoder, const double* llrs, int64_t frames,
+                         double alpha, int32_t max_iter, pbp_frame_out* out) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    if (frames < 0) return fail(PBP_EINVAL, "frames < 0");
+    PBP_CUDA(cudaSetDevice(ctx->device));
+    int rc = upload_code(ctx, code);
+    if (rc) return rc;
+    const int n = ctx->n, nw = (n + 31) / 32;
+    if ((rc = ctx->llr64.ensure((size_t)frames * n)) || (rc = ctx->ubits.ensure((size_t)frames * nw)) ||
+        (rc = ctx->iters.ensure(frames)) || (rc = ctx->pe.ensure(frames)) ||
+        (rc = ctx->stop.ensure(frames)) || (rc = ctx->nev.ensure(frames)))
+        return rc;
+    cudaStream_t st = ctx->stream;
+    if (frames > 0)
+        PBP_CUDA(cudaMemcpyAsync(ctx->llr64.p, llrs, (size_t)frames * n * 8, cudaMemcpyHostToDevice, st));
+    DecodeReq r;
+    r.kind = decoder;
+    r.llr64 = ctx->llr64.p;
+    r.alpha64 = alpha;
+    r.frames = frames;
+    r.max_iter = max_iter;
+    r.u_bits = ctx->ubits.p;
+    r.iters = ctx->iters.p;
+    r.pe = ctx->pe.p;
+    r.stop = ctx->stop.p;
+    r.nev = ctx->nev.p;
+    if ((rc = begin_call(ctx, 1))) return rc;
+    if ((rc = run_decode(ctx, r, ctx->slot[0], st))) return rc;
+    if (out && frames > 0) {
+        if (out->u_hat_bits)
+            PBP_CUDA(cudaMemcpyAsync(out->u_hat_bits, r.u_bits, (size_t)frames * nw * 4, cudaMemcpyDeviceToHost, st));
+        if (out->iterations)
+            PBP_CUDA(cudaMemcpyAsync(out->iterations, r.iters, (size_t)frames * 4, cudaMemcpyDeviceToHost, st));
+        if (out->pe) PBP_CUDA(cudaMemcpyAsync(out->pe, r.pe, (size_t)frames * 8, cudaMemcpyDeviceToHost, st));
+        if (out->stop) PBP_CUDA(cudaMemcpyAsync(out->stop, r.stop, (size_t)frames, cudaMemcpyDeviceToHost, st));
+        if (out->n_events)
+            PBP_CUDA(cudaMemcpyAsync(out->n_events, r.nev, (size_t)frames * 4, cudaMemcpyDeviceToHost, st));
+    }
+    PBP_CUDA(cudaStreamSynchronize(st));
     return PBP_OK;
 }
 
@@ -768,9 +871,11 @@ int pbp_decode_count_device(pbp_ctx* ctx, const pbp_code* code, int decoder, con
     return run_decode(ctx, r, ctx->slot[0], pick(ctx, stream));
 }
 
-int pbp_simulate_point_device(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed,
-                              int64_t first_trial, int64_t frames, double ebn0_db, int noiseless,
-                              float alpha, int32_t max_iter, int64_t* counters_dev, void* stream) {
+// run_point's trial loop on the device: fp32 LLRs (the fast path) or, with
+// f64, the reference's double LLRs decoded in double.
+static int simulate_point_impl(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed,
+                               int64_t first_trial, int64_t frames, double ebn0_db, int noiseless, double alpha,
+                               bool f64, int32_t max_iter, int64_t* counters_dev, void* stream) {
     if (!ctx) return fail(PBP_EINVAL, "null context");
     if (frames < 0) return fail(PBP_EINVAL, "frames < 0");
     PBP_CUDA(cudaSetDevice(ctx->device));
@@ -780,18 +885,24 @@ int pbp_simulate_point_device(pbp_ctx* ctx, const pbp_code* code, int decoder, u
     // chunk so the staging stays bounded (~256 MiB of LLRs)
     const long long chunk = std::max<long long>(1, std::min<long long>(frames, (1ll << 26) / n));
     if ((rc = ctx->llr.ensure((size_t)chunk * n)) || (rc = ctx->truth.ensure((size_t)chunk * nw))) return rc;
+    if (f64 && (rc = ctx->llr64.ensure((size_t)chunk * n))) return rc;
     cudaStream_t st = pick(ctx, stream);
     if ((rc = begin_call(ctx, (int)((frames + chunk - 1) / chunk)))) return rc;
     for (long long done = 0; done < frames; done += chunk) {
         const long long c = std::min(chunk, frames - done);
-        if ((rc = run_generate(ctx, seed, first_trial + done, c, ebn0_db, noiseless, ctx->llr.p, nullptr,
-                               ctx->truth.p, st)))
+        if ((rc = run_generate(ctx, seed, first_trial + done, c, ebn0_db, noiseless, ctx->llr.p,
+                               f64 ? ctx->llr64.p : nullptr, ctx->truth.p, st)))
             return rc;
         DecodeReq r;
         r.kind = decoder;
-        r.llr = ctx->llr.p;
+        if (f64) {
+            r.llr64 = ctx->llr64.p;
+            r.alpha64 = alpha;
+        } else {
+            r.llr = ctx->llr.p;
+            r.alpha = (float)alpha;
+        }
         r.frames = c;
-        r.alpha = alpha;
         r.max_iter = max_iter;
         r.truth = ctx->truth.p;
         r.counters = reinterpret_cast<unsigned long long*>(counters_dev);
@@ -800,16 +911,23 @@ int pbp_simulate_point_device(pbp_ctx* ctx, const pbp_code* code, int decoder, u
     return PBP_OK;
 }
 
-int pbp_simulate_point(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed, int64_t first_trial,
-                       int64_t frames, double ebn0_db, int noiseless, float alpha, int32_t max_iter,
-                       pbp_counters* out) {
+int pbp_simulate_point_device(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed,
+                              int64_t first_trial, int64_t frames, double ebn0_db, int noiseless,
+                              float alpha, int32_t max_iter, int64_t* counters_dev, void* stream) {
+    return simulate_point_impl(ctx, code, decoder, seed, first_trial, frames, ebn0_db, noiseless, alpha, false,
+                               max_iter, counters_dev, stream);
+}
+
+static int simulate_point_host(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed, int64_t first_trial,
+                               int64_t frames, double ebn0_db, int noiseless, double alpha, bool f64,
+                               int32_t max_iter, pbp_counters* out) {
     if (!ctx || !out) return fail(PBP_EINVAL, "null argument");
     PBP_CUDA(cudaSetDevice(ctx->device));
     int rc;
     if ((rc = ctx->counters.ensure(pbp::kNumCounters))) return rc;
     PBP_CUDA(cudaMemsetAsync(ctx->counters.p, 0, pbp::kNumCounters * 8, ctx->stream));
-    rc = pbp_simulate_point_device(ctx, code, decoder, seed, first_trial, frames, ebn0_db, noiseless, alpha,
-                                   max_iter, reinterpret_cast<int64_t*>(ctx->counters.p), ctx->stream);
+    rc = simulate_point_impl(ctx, code, decoder, seed, first_trial, frames, ebn0_db, noiseless, alpha, f64,
+                             max_iter, reinterpret_cast<int64_t*>(ctx->counters.p), ctx->stream);
     if (rc) return rc;
     unsigned long long c[pbp::kNumCounters];
     PBP_CUDA(cudaMemcpyAsync(c, ctx->counters.p, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
@@ -823,6 +941,20 @@ int pbp_simulate_point(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t
     out->sum_events = (int64_t)c[pbp::kCntEvents];
     for (int i = 0; i < 3; ++i) out->stop_hist[i] = (int64_t)c[pbp::kCntStop0 + i];
     return PBP_OK;
+}
+
+int pbp_simulate_point(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed, int64_t first_trial,
+                       int64_t frames, double ebn0_db, int noiseless, float alpha, int32_t max_iter,
+                       pbp_counters* out) {
+    return simulate_point_host(ctx, code, decoder, seed, first_trial, frames, ebn0_db, noiseless, alpha, false,
+                               max_iter, out);
+}
+
+int pbp_simulate_point_f64(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed, int64_t first_trial,
+                           int64_t frames, double ebn0_db, int noiseless, double alpha, int32_t max_iter,
+                           pbp_counters* out) {
+    return simulate_point_host(ctx, code, decoder, seed, first_trial, frames, ebn0_db, noiseless, alpha, true,
+                               max_iter, out);
 }
 
 }  // extern "C"

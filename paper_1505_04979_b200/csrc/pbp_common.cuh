@@ -28,6 +28,8 @@ struct DecodeArgs {
     const uint32_t* frozen_bits;  // device, ceil(n/32) words
     const uint8_t* frozen_rows;   // device, n bytes
     const float* llr;             // frames x n
+    const double* llr64;          // frames x n: decode in fp64 (generic kernel only)
+    double alpha64;
     long long frames;
     // per-frame outputs (device, nullable)
     uint32_t* u_bits;

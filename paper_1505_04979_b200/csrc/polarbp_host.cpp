@@ -266,6 +266,29 @@ std::vector<double> transmit_awgn(std::span<const double> symbols, const Channel
     return llr;
 }
 
+namespace {
+void unpack_u(const PolarCode& code, std::int64_t count, const std::vector<uint32_t>& ub, std::vector<Bits>* u_words) {
+    const int nw = (code.n + 31) / 32;
+    if (u_words) {
+        u_words->assign(count, Bits(code.n));
+        for (std::int64_t f = 0; f < count; ++f)
+            for (int r = 0; r < code.n; ++r) (*u_words)[f][r] = (ub[f * nw + (r >> 5)] >> (r & 31)) & 1u;
+    }
+}
+}  // namespace
+
+void generate_frames(const PolarCode& code, std::uint64_t seed, std::int64_t first_trial, std::int64_t count,
+                     const ChannelConfig& config, std::vector<double>& llrs, std::vector<Bits>* u_words) {
+    const pbp_code v = view(code);
+    const int nw = (code.n + 31) / 32;
+    llrs.assign(static_cast<size_t>(count) * code.n, 0.0);
+    std::vector<float> l32(static_cast<size_t>(count) * code.n);
+    std::vector<uint32_t> ub(static_cast<size_t>(count) * nw);
+    raise(pbp_generate(ctx(), &v, seed, first_trial, count, config.ebn0_db, config.noiseless ? 1 : 0, l32.data(),
+                       llrs.data(), ub.data()));
+    unpack_u(code, count, ub, u_words);
+}
+
 void generate_frames(const PolarCode& code, std::uint64_t seed, std::int64_t first_trial, std::int64_t count,
                      const ChannelConfig& config, std::vector<float>& llrs, std::vector<Bits>* u_words) {
     const pbp_code v = view(code);
@@ -305,10 +328,11 @@ const char* to_string(StopReason reason) {
 
 namespace {
 
-DecodeOutcome one_frame(const PolarCode& code, int kind, std::span<const double> llrs, double alpha, int max_iter,
+// one frame with its freeze-event trace: T = double (as shipped) or float (the fp32 path)
+template <typename T>
+DecodeOutcome one_frame(const PolarCode& code, int kind, std::span<const T> llrs, double alpha, int max_iter,
                         std::vector<FreezeEvent>* events) {
     if (static_cast<int>(llrs.size()) != code.n) throw std::invalid_argument("init_state: LLR length != n");
-    std::vector<float> l32(llrs.begin(), llrs.end());
     const pbp_code v = view(code);
     DecodeOutcome out;
     out.u_hat.assign(code.n, 0);
@@ -316,8 +340,12 @@ DecodeOutcome one_frame(const PolarCode& code, int kind, std::span<const double>
     int64_t pe = 0;
     const int cap = 4096;
     std::vector<int32_t> ev(events ? static_cast<size_t>(cap) * 5 : 5);
-    raise(pbp_decode_trace(ctx(), &v, kind, l32.data(), static_cast<float>(alpha), max_iter, out.u_hat.data(), &it,
-                           &pe, &stop, &nev, ev.data(), events ? cap : 1));
+    if constexpr (sizeof(T) == 8)
+        raise(pbp_decode_trace_f64(ctx(), &v, kind, llrs.data(), alpha, max_iter, out.u_hat.data(), &it, &pe, &stop,
+                                   &nev, ev.data(), events ? cap : 1));
+    else
+        raise(pbp_decode_trace(ctx(), &v, kind, llrs.data(), static_cast<float>(alpha), max_iter, out.u_hat.data(),
+                               &it, &pe, &stop, &nev, ev.data(), events ? cap : 1));
     out.info_bits = extract_info_bits(code, out.u_hat);
     out.iterations_used = it;
     out.pe_activations = pe;
@@ -333,20 +361,22 @@ DecodeOutcome one_frame(const PolarCode& code, int kind, std::span<const double>
 }  // namespace
 
 DecodeOutcome decode_baseline(const PolarCode& code, std::span<const double> llrs, double alpha, int max_iter) {
-    return one_frame(code, PBP_BASELINE, llrs, alpha, max_iter, nullptr);
+    return one_frame<double>(code, PBP_BASELINE, llrs, alpha, max_iter, nullptr);
 }
 
 DecodeOutcome decode_gmatrix(const PolarCode& code, std::span<const double> llrs, double alpha, int max_iter) {
-    return one_frame(code, PBP_GMATRIX, llrs, alpha, max_iter, nullptr);
+    return one_frame<double>(code, PBP_GMATRIX, llrs, alpha, max_iter, nullptr);
 }
 
 DecodeOutcome decode_csfg(const PolarCode& code, std::span<const double> llrs, double alpha, int max_iter,
                           std::vector<FreezeEvent>* events) {
-    return one_frame(code, PBP_CSFG, llrs, alpha, max_iter, events);
+    return one_frame<double>(code, PBP_CSFG, llrs, alpha, max_iter, events);
 }
 
-std::vector<DecodeOutcome> decode_batch(const PolarCode& code, BatchDecoder decoder, std::span<const float> llrs,
-                                        double alpha, int max_iter) {
+namespace {
+template <typename T>
+std::vector<DecodeOutcome> batch_impl(const PolarCode& code, BatchDecoder decoder, std::span<const T> llrs,
+                                      double alpha, int max_iter) {
     if (llrs.size() % code.n) throw std::invalid_argument("init_state: LLR length != n");
     const int64_t frames = static_cast<int64_t>(llrs.size() / code.n);
     const int nw = (code.n + 31) / 32;
@@ -356,8 +386,11 @@ std::vector<DecodeOutcome> decode_batch(const PolarCode& code, BatchDecoder deco
     std::vector<uint8_t> stop(frames);
     pbp_frame_out fo{ub.data(), it.data(), pe.data(), stop.data(), nev.data()};
     const pbp_code v = view(code);
-    raise(pbp_decode_batch(ctx(), &v, static_cast<int>(decoder), llrs.data(), frames, static_cast<float>(alpha),
-                           max_iter, &fo));
+    if constexpr (sizeof(T) == 8)
+        raise(pbp_decode_batch_f64(ctx(), &v, static_cast<int>(decoder), llrs.data(), frames, alpha, max_iter, &fo));
+    else
+        raise(pbp_decode_batch(ctx(), &v, static_cast<int>(decoder), llrs.data(), frames, static_cast<float>(alpha),
+                               max_iter, &fo));
     std::vector<DecodeOutcome> out(frames);
     for (int64_t f = 0; f < frames; ++f) {
         out[f].u_hat.resize(code.n);
@@ -368,6 +401,17 @@ std::vector<DecodeOutcome> decode_batch(const PolarCode& code, BatchDecoder deco
         out[f].stop_reason = static_cast<StopReason>(stop[f]);
     }
     return out;
+}
+}  // namespace
+
+std::vector<DecodeOutcome> decode_batch(const PolarCode& code, BatchDecoder decoder, std::span<const float> llrs,
+                                        double alpha, int max_iter) {
+    return batch_impl<float>(code, decoder, llrs, alpha, max_iter);
+}
+
+std::vector<DecodeOutcome> decode_batch(const PolarCode& code, BatchDecoder decoder, std::span<const double> llrs,
+                                        double alpha, int max_iter) {
+    return batch_impl<double>(code, decoder, llrs, alpha, max_iter);
 }
 
 BlockRef candidate_block(int n, int frontier, int stage) {
@@ -456,19 +500,32 @@ std::vector<PointStats> run_point(const SimConfig& cfg, double snr_db, const Tra
     while (frames < cfg.max_frames) {
         const long long c = std::min(chunk, cfg.max_frames - frames);
         std::vector<float> llr;
+        std::vector<double> llr64;
         std::vector<Bits> u;
-        generate_frames(code, cfg.seed, frames, c, ch, llr, &u);
+        if (cfg.fp64)
+            generate_frames(code, cfg.seed, frames, c, ch, llr64, &u);
+        else
+            generate_frames(code, cfg.seed, frames, c, ch, llr, &u);
         std::vector<std::vector<DecodeOutcome>> outs(nd);
         for (size_t d = 0; d < nd; ++d) {
+            const auto kind = static_cast<BatchDecoder>(cfg.decoders[d]);
             if (trace && cfg.decoders[d] == DecoderKind::csfg) {
                 for (long long f = 0; f < c; ++f) {
-                    std::vector<double> l64(llr.begin() + f * code.n, llr.begin() + (f + 1) * code.n);
                     std::vector<FreezeEvent> ev;
-                    outs[d].push_back(decode_csfg(code, l64, cfg.alpha, cfg.max_iter, &ev));
+                    if (cfg.fp64)
+                        outs[d].push_back(one_frame<double>(
+                            code, PBP_CSFG, std::span<const double>(llr64.data() + f * code.n, code.n), cfg.alpha,
+                            cfg.max_iter, &ev));
+                    else
+                        outs[d].push_back(one_frame<float>(
+                            code, PBP_CSFG, std::span<const float>(llr.data() + f * code.n, code.n), cfg.alpha,
+                            cfg.max_iter, &ev));
                     for (const auto& e : ev) (*trace)(frames + f, e);
                 }
+            } else if (cfg.fp64) {
+                outs[d] = decode_batch(code, kind, std::span<const double>(llr64), cfg.alpha, cfg.max_iter);
             } else {
-                outs[d] = decode_batch(code, static_cast<BatchDecoder>(cfg.decoders[d]), llr, cfg.alpha, cfg.max_iter);
+                outs[d] = decode_batch(code, kind, std::span<const float>(llr), cfg.alpha, cfg.max_iter);
             }
         }
         // merge in trial order, stop rule on 256-frame batch boundaries
