@@ -6,9 +6,11 @@
 // each stage (src/csfg_freeze.cpp:107-119) and the G-check after each
 // sweep (src/bp_core.cpp:95-102, src/csfg_freeze.cpp:120-135). Every clamp,
 // sgn(0)=+1 and std::min tie rule of pe_update (src/bp_core.cpp:13-32) is
-// kept, so it is exact for any finite or non-finite LLR. Messages live in a
-// per-CTA global scratch region (L2 resident for the configs), bit-level
-// state in shared memory.
+// kept, so it is exact for any finite or non-finite LLR. Messages L(1..m)
+// and the current R level live in shared memory when they fit (n <= 4096 in
+// fp32: 13 x 16 KB, one 512-thread CTA per SM), else in a per-CTA global
+// scratch region; R(0) is read from the LLR input (clamped) and L(0) is only
+// kept as the G-check's hard-decision bits, formed at stage 0.
 //
 // Roles: (1) the decode path for n outside the warp-resident kernel's range
 // (n < 128 and n >= 2048), (2) the path for frames the fast kernel
@@ -67,17 +69,25 @@ __device__ void cta_transform(uint32_t* words, int nbits) {
 
 }  // namespace
 
-template <int BLOCK, typename T>
+// shared words ahead of the message arrays: decided_u, two scratch bit
+// vectors, stage-0 hard decisions, freeze_stage bytes
+__host__ __device__ inline size_t generic_bits_bytes(int n) {
+    const size_t nw = (size_t)(n + 31) / 32;
+    return (4 * nw * 4 + (size_t)n + 15) / 16 * 16;
+}
+
+template <int BLOCK, typename T, bool SM>
 __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
     using O = RealOps<T>;
     const T cap = O::cap;
-    extern __shared__ uint32_t smem[];
+    extern __shared__ __align__(16) uint32_t smem[];
     const int n = a.n, m = a.m;
     const int nw_all = (n + 31) >> 5;
     uint32_t* dec_u = smem;               // decided_u bits
     uint32_t* wb0 = smem + nw_all;        // scratch words
     uint32_t* wb1 = smem + 2 * nw_all;    // scratch words
-    uint8_t* fst = reinterpret_cast<uint8_t*>(smem + 3 * nw_all);  // freeze_stage per row
+    uint32_t* xh = smem + 3 * nw_all;     // x_hat = (R(0) + L(0) < 0) of the last sweep
+    uint8_t* fst = reinterpret_cast<uint8_t*>(smem + 4 * nw_all);  // freeze_stage per row
 
     __shared__ long long s_frame;
     __shared__ int s_frontier, s_nev;
@@ -86,10 +96,10 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    T* L = reinterpret_cast<T*>(a.scratch) + (long long)blockIdx.x * a.scratch_stride;  // (m+1) x n
-    T* R0 = L + (size_t)(m + 1) * n;
-    T* R = R0 + n;
-    const T* Rm = (m == 0) ? R0 : R;
+    // L(s) for s = 1..m at L + (s-1) n, then the current R level
+    T* L = SM ? reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(smem) + generic_bits_bytes(n))
+              : reinterpret_cast<T*>(a.scratch) + (long long)blockIdx.x * a.scratch_stride;
+    T* R = L + (size_t)m * n;
     const T alpha = sizeof(T) == 8 ? T(a.alpha64) : T(a.alpha);
     const bool csfg = a.kind == 2;
 
@@ -113,11 +123,14 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
         if (frame < 0) break;
 
         // init_state (src/bp_core.cpp:43-56)
+        // R(0) = clamp(LLR), read where needed (src/bp_core.cpp:47)
+        const float* llr32 = a.llr + frame * (long long)n;
+        const double* llr64 = sizeof(T) == 8 ? a.llr64 + frame * (long long)n : nullptr;
+        auto R0 = [&](int r) -> T { return ref_clamp(sizeof(T) == 8 ? T(llr64[r]) : T(llr32[r])); };
         for (int r = tid; r < n; r += BLOCK) {
-            const T v = sizeof(T) == 8 ? T(a.llr64[frame * (long long)n + r]) : T(a.llr[frame * (long long)n + r]);
-            R0[r] = ref_clamp(v);
-            for (int s = 0; s < m; ++s) L[(size_t)s * n + r] = T(0);
-            L[(size_t)m * n + r] = a.frozen_rows[r] ? cap : T(0);
+            for (int s = 1; s < m; ++s) L[(size_t)(s - 1) * n + r] = T(0);
+            if (m > 0) L[(size_t)(m - 1) * n + r] = a.frozen_rows[r] ? cap : T(0);
+            R[r] = T(0);
             fst[r] = kNotFrozen;
         }
         for (int q = tid; q < nw_all; q += BLOCK) dec_u[q] = 0u;
@@ -136,20 +149,50 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
                 // ---- stage_pass (src/bp_core.cpp:58-80) ----
                 const int ld = m - 1 - s;
                 const int d = 1 << ld;
-                const T* Rin = (s == 0) ? R0 : R;
-                T* Ls = L + (size_t)s * n;
-                const T* Ls1 = L + (size_t)(s + 1) * n;
-                for (int p = tid; p < n / 2; p += BLOCK) {
-                    const int r = ((p >> ld) << (ld + 1)) | (p & (d - 1));
-                    if (csfg && (int)fst[r] < s) continue;  // is_pe_active (csfg_freeze.cpp:95-97)
-                    const T lt = Ls1[r], lb = Ls1[r + d], rt = Rin[r], rb = Rin[r + d];
-                    const T cross = ref_f(alpha, lt, rt);
-                    const T sum_bot = O::add(lb, rb);
-                    Ls[r] = ref_clamp(ref_f(alpha, lt, sum_bot));
-                    Ls[r + d] = ref_clamp(O::add(lb, cross));
-                    R[r] = ref_clamp(ref_f(alpha, rt, sum_bot));
-                    R[r + d] = ref_clamp(O::add(rb, cross));
-                    ++act;
+                T* Ls = (s > 0) ? L + (size_t)(s - 1) * n : nullptr;
+                const T* Ls1 = L + (size_t)s * n;
+                if (s == 0 && n < 64)
+                    for (int q = tid; q < nw_all; q += BLOCK) xh[q] = 0u;
+                if (s == 0) __syncthreads();
+                for (int p0 = 0; p0 < n / 2; p0 += BLOCK) {
+                    const int p = p0 + tid;
+                    bool xt = false, xbot = false;
+                    int r = 0;
+                    if (p < n / 2) {
+                        r = ((p >> ld) << (ld + 1)) | (p & (d - 1));
+                        // is_pe_active (csfg_freeze.cpp:95-97); stage 0 is always active
+                        if (!(csfg && (int)fst[r] < s)) {
+                            const T lt = Ls1[r], lb = Ls1[r + d];
+                            const T rt = (s == 0) ? R0(r) : R[r], rb = (s == 0) ? R0(r + d) : R[r + d];
+                            const T cross = ref_f(alpha, lt, rt);
+                            const T sum_bot = O::add(lb, rb);
+                            const T l_top = ref_clamp(ref_f(alpha, lt, sum_bot));
+                            const T l_bot = ref_clamp(O::add(lb, cross));
+                            if (s > 0) {
+                                Ls[r] = l_top;
+                                Ls[r + d] = l_bot;
+                            } else {  // L(0) only feeds the G-check's x_hat (bp_core.cpp:99)
+                                xt = O::add(rt, l_top) < T(0);
+                                xbot = O::add(rb, l_bot) < T(0);
+                            }
+                            R[r] = ref_clamp(ref_f(alpha, rt, sum_bot));
+                            R[r + d] = ref_clamp(O::add(rb, cross));
+                            ++act;
+                        }
+                    }
+                    if (s == 0) {
+                        if (n >= 64) {  // rows r = p and r + n/2: whole warps of consecutive rows
+                            const uint32_t wt = __ballot_sync(0xffffffffu, xt);
+                            const uint32_t wbt = __ballot_sync(0xffffffffu, xbot);
+                            if (lane == 0 && p < n / 2) {
+                                xh[r >> 5] = wt;
+                                xh[(r + d) >> 5] = wbt;
+                            }
+                        } else if (p < n / 2) {
+                            if (xt) atomicOr(&xh[r >> 5], 1u << (r & 31));
+                            if (xbot) atomicOr(&xh[(r + d) >> 5], 1u << ((r + d) & 31));
+                        }
+                    }
                 }
                 __syncthreads();
                 if (!csfg) continue;
@@ -180,7 +223,7 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
                 if (accept) {
                     for (int i = tid; i < sz; i += BLOCK) {
                         const int r = start + i;
-                        L[(size_t)(s + 1) * n + r] = (R[r] < T(0)) ? -cap : cap;
+                        L[(size_t)s * n + r] = (R[r] < T(0)) ? -cap : cap;  // L(s+1)
                         if ((int)fst[r] > s) fst[r] = (uint8_t)s;
                     }
                     if (sz >= 32) {
@@ -212,17 +255,14 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
             // ---- gmatrix_converged (src/bp_core.cpp:95-102), pinned prefix
             //      for csfg (src/csfg_freeze.cpp:120-135) ----
             for (int i = tid; i < nw_all * 32; i += BLOCK) {
-                bool ub = false, xb = false;
-                if (i < n) {
+                bool ub = false;
+                if (i < n)
                     ub = (i < pin) ? ((dec_u[i >> 5] >> (i & 31)) & 1u)
-                                   : (!a.frozen_rows[i] && Rm[i] < T(0));
-                    xb = O::add(R0[i], L[i]) < T(0);
-                }
+                                   : (!a.frozen_rows[i] && R[i] < T(0));
                 const uint32_t wu = __ballot_sync(0xffffffffu, ub);
-                const uint32_t wx = __ballot_sync(0xffffffffu, xb);
                 if (lane == 0) {
                     wb0[i >> 5] = wu;
-                    wb1[i >> 5] = wx;
+                    wb1[i >> 5] = xh[i >> 5] & low_mask(n - (i & ~31));
                 }
             }
             __syncthreads();
@@ -248,7 +288,7 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
             bool ub = false;
             if (i < n)
                 ub = (i < pin) ? ((dec_u[i >> 5] >> (i & 31)) & 1u)
-                               : (!a.frozen_rows[i] && Rm[i] < T(0));
+                               : (!a.frozen_rows[i] && (m == 0 ? R0(i) : R[i]) < T(0));
             const uint32_t w = __ballot_sync(0xffffffffu, ub);
             if (lane == 0) {
                 if (a.u_bits) a.u_bits[frame * nw_all + (i >> 5)] = w;
@@ -282,34 +322,50 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
 }
 
 // Host-side launch helpers (called from pbp_capi.cu)
-constexpr int kGenericBlock = 256;
+constexpr int kGenericBlock = 256;     // messages in global scratch
+constexpr int kGenericBlockSM = 512;   // messages in shared memory
+constexpr size_t kMaxSmem = 227 * 1024;
 
-size_t generic_smem_bytes(int n) {
-    const int nw = (n + 31) / 32;
-    return (size_t)3 * nw * 4 + (size_t)n + 16;
+static size_t smem_state_bytes(int n, int m, size_t esz) {
+    return generic_bits_bytes(n) + (size_t)(m + 1) * n * esz;
 }
 
-// per-CTA message scratch in elements of the decode precision (float or
-// double); scratch_stride is in those elements
+// Messages in shared memory when at least four frames fit per SM: the kernel
+// is bound by its per-stage barriers, so frames per SM matter more than the
+// memory level (n = 4096 in shared memory, one frame per SM, measured 18 %
+// slower than L2-resident scratch with eight frames per SM).
+bool generic_in_smem(int n, int m, bool f64) {
+    return smem_state_bytes(n, m, f64 ? 8 : 4) <= kMaxSmem / 4;
+}
+
+size_t generic_smem_bytes(int n) { return generic_bits_bytes(n); }
+
+// per-CTA message scratch (global variant) in elements of the decode
+// precision: L(1..m) and the current R level
 long long generic_scratch_elems(int n, int m) {
-    long long f = (long long)(m + 3) * n;
+    long long f = (long long)(m + 1) * n;
     return (f + 63) / 64 * 64;
 }
 
-template <typename T>
+template <int BLOCK, typename T, bool SM>
 static cudaError_t launch_t(const DecodeArgs& a, int grid, cudaStream_t stream) {
-    const size_t smem = generic_smem_bytes(a.n);
+    const size_t smem = SM ? smem_state_bytes(a.n, a.m, sizeof(T)) : generic_bits_bytes(a.n);
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(bp_generic_kernel<kGenericBlock, T>,
+        cudaError_t e = cudaFuncSetAttribute(bp_generic_kernel<BLOCK, T, SM>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    bp_generic_kernel<kGenericBlock, T><<<grid, kGenericBlock, smem, stream>>>(a);
+    bp_generic_kernel<BLOCK, T, SM><<<grid, BLOCK, smem, stream>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_generic(const DecodeArgs& a, int grid, cudaStream_t stream) {
-    return a.llr64 ? launch_t<double>(a, grid, stream) : launch_t<float>(a, grid, stream);
+    const bool f64 = a.llr64 != nullptr;
+    if (generic_in_smem(a.n, a.m, f64))
+        return f64 ? launch_t<kGenericBlockSM, double, true>(a, grid, stream)
+                   : launch_t<kGenericBlockSM, float, true>(a, grid, stream);
+    return f64 ? launch_t<kGenericBlock, double, false>(a, grid, stream)
+               : launch_t<kGenericBlock, float, false>(a, grid, stream);
 }
 
 }  // namespace pbp

@@ -19,6 +19,7 @@ namespace pbp {
 cudaError_t launch_generic(const DecodeArgs& a, int grid, cudaStream_t stream);
 size_t generic_smem_bytes(int n);
 long long generic_scratch_elems(int n, int m);
+bool generic_in_smem(int n, int m, bool f64);
 cudaError_t launch_warp(const DecodeArgs& a, int grid, cudaStream_t st);
 int warp_kernel_supported(int m);
 int warp_blocks_per_sm(int m, int kind);
@@ -214,6 +215,7 @@ int size_slot(pbp_ctx* ctx, DecodeSlot& s, int kind, long long frames) {
         if ((rc = s.r0s.ensure((size_t)(grid * ctx->n)))) return rc;
     }
     const bool fast = !ctx->force_generic && pbp::warp_kernel_supported(ctx->m);
+    if (pbp::generic_in_smem(ctx->n, ctx->m, false)) return PBP_OK;
     return s.scratch.ensure((size_t)generic_grid(ctx, frames, fast) * pbp::generic_scratch_elems(ctx->n, ctx->m));
 }
 
@@ -275,9 +277,11 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
     const int esz = r.llr64 ? 2 : 1;  // in floats
     const long long stride = pbp::generic_scratch_elems(ctx->n, ctx->m);
     const long long grid = generic_grid(ctx, r.frames, fast, esz);
-    if ((rc = s.scratch.ensure((size_t)(grid * stride * esz)))) return rc;
-    a.scratch = s.scratch.p;
-    a.scratch_stride = stride;
+    if (!pbp::generic_in_smem(ctx->n, ctx->m, r.llr64 != nullptr)) {
+        if ((rc = s.scratch.ensure((size_t)(grid * stride * esz)))) return rc;
+        a.scratch = s.scratch.p;
+        a.scratch_stride = stride;
+    }
     cudaError_t e = pbp::launch_generic(a, (int)grid, st);
     if (e != cudaSuccess) return cuda_fail(e, "bp_generic_kernel launch");
     ctx->last_launches += 1;
@@ -320,9 +324,11 @@ int run_generic_list(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream
     a.queue = s.ctl.p + 1;
     const long long stride = pbp::generic_scratch_elems(ctx->n, ctx->m);
     const long long grid = generic_grid(ctx, std::max<long long>(1, listed), false);
-    if ((rc = s.scratch.ensure((size_t)(grid * stride)))) return rc;
-    a.scratch = s.scratch.p;
-    a.scratch_stride = stride;
+    if (!pbp::generic_in_smem(ctx->n, ctx->m, false)) {
+        if ((rc = s.scratch.ensure((size_t)(grid * stride)))) return rc;
+        a.scratch = s.scratch.p;
+        a.scratch_stride = stride;
+    }
     cudaError_t e = pbp::launch_generic(a, (int)grid, st);
     if (e != cudaSuccess) return cuda_fail(e, "bp_generic_kernel launch");
     ctx->last_launches += 1;
