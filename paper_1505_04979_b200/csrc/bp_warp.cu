@@ -582,7 +582,8 @@ struct Dec {
     struct LastWalk {
         int A5;               // window start
         uint32_t x[PL::NL];   // window sign bits per last-pass stage (uniform)
-        int A[PL::NL];        // block start of stage SL + t's candidate
+        int E[PL::NL];        // block end of stage SL + t's commit (blocks tile [A0, frontier))
+        int A0;               // start of the first commit's block
         uint32_t xl, ul;      // lane t: x_hat / u_hat bits of the window at stage SL + t
         int Al;               // lane t: A[t]
         uint32_t cmask;       // bit t: stage SL + t committed
@@ -622,24 +623,27 @@ struct Dec {
         for (int tp = 0; tp < K - 1; ++tp)
             if (tp < g) viol |= viol >> (1 << tp);
         // the reference's stage loop over the last pass
-        int F = frontier;
+        int F = frontier, slast = s_last_, A0 = N;
+        uint32_t cm = 0u;
         bool done = false;
 #pragma unroll
         for (int t = 0; t < NL; ++t) {
             const uint32_t vt = __shfl_sync(kFull, viol, t);
             const int gt = M - 1 - (SL + t);
             const int A = (F >> gt) << gt;
-            w.A[t] = A;
             if (lane == t) w.Al = A;
-            if (!done && !((vt >> (A - w.A5)) & 1u)) {
-                w.cmask |= 1u << t;
-                F = A + (1 << gt);
-                if (F >= N) {
-                    s_last_ = SL + t;
-                    done = true;
-                }
-            }
+            const bool acc = !done && !((vt >> (A - w.A5)) & 1u);
+            cm |= (uint32_t)acc << t;
+            A0 = (acc && cm == (1u << t)) ? A : A0;  // first commit's block start
+            F = acc ? A + (1 << gt) : F;
+            w.E[t] = F;                              // end of stage t's block when it commits
+            const bool fin = acc && F >= N;
+            slast = fin ? SL + t : slast;
+            done = done || fin;
         }
+        w.cmask = cm;
+        w.A0 = A0;
+        s_last_ = slast;
         frontier = F;
         done_ = done;
     }
@@ -789,14 +793,15 @@ struct Dec {
         const int r = w.A5 + lane;
         int Sr = -1;
         uint32_t xbit = 0u;
+        // row r >= A0 belongs to the earliest committed stage whose block ends after it
 #pragma unroll
-        for (int t = 0; t < NL; ++t) {
-            const int gt = M - 1 - (SL + t);
-            if (((cmask >> t) & 1u) && r >= w.A[t] && r < w.A[t] + (1 << gt)) {
+        for (int t = NL - 1; t >= 0; --t) {
+            if (((cmask >> t) & 1u) && r < w.E[t]) {
                 Sr = SL + t;
                 xbit = (w.x[t] >> lane) & 1u;
             }
         }
+        if (r < w.A0) Sr = -1;
         int fo = kNotFrozen;
         if (Sr >= 0) fo = sm->fst[r];
         if (nce == 0) {
