@@ -82,7 +82,28 @@ def build(verbose=False, jobs=None):
         if verbose:
             print(" ".join(link), flush=True)
         subprocess.run(link, check=True)
+    build_cli(verbose)
     return LIB
+
+
+CLI_SRC = os.path.join(PKG, "cli", "polarbp_cli.cpp")
+CLI = os.path.join(LIB_DIR, "polarbp")
+
+
+def build_cli(verbose=False):
+    """The `polarbp` command (reference tools/polarbp_main.cpp) linked to libpbp.so."""
+    if os.environ.get("PBP_LIB_NAME"):  # experiment builds: library only
+        return None
+    deps = [CLI_SRC, LIB] + [os.path.join(ROOT, "include", "polarbp", f)
+                             for f in os.listdir(os.path.join(ROOT, "include", "polarbp"))]
+    if os.path.exists(CLI) and all(os.path.getmtime(d) <= os.path.getmtime(CLI) for d in deps):
+        return CLI
+    cmd = ["g++", "-O2", "-std=c++20", "-I", os.path.join(ROOT, "include"), CLI_SRC, "-L", LIB_DIR, "-lpbp",
+           "-Wl,-rpath,$ORIGIN", "-o", CLI]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    return CLI
 
 
 if __name__ == "__main__":
