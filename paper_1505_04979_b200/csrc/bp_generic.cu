@@ -51,19 +51,18 @@ template <typename T> __device__ __forceinline__ T ref_f(T alpha, T a, T b) {
     return O::mul(O::mul(O::mul(alpha, ref_sgn(a)), ref_sgn(b)), ref_min(O::abs(a), O::abs(b)));
 }
 
-// Polar transform of `nbits` bits held in words[0..ceil(nbits/32)) of
-// shared memory, by the whole CTA (polar_code.cpp:13-20 on packed words).
-template <int BLOCK>
-__device__ void cta_transform(uint32_t* words, int nbits) {
+// Polar transform (polar_code.cpp:13-20) of `nbits` bits held in words[0..ceil(nbits/32))
+// of shared memory, by one warp (no CTA barrier between the butterfly levels).
+__device__ void warp_transform(uint32_t* words, int nbits, int lane) {
     const int nw = (nbits + 31) >> 5;
-    for (int q = threadIdx.x; q < nw; q += BLOCK) words[q] = word_transform(words[q], nbits);
-    __syncthreads();
+    for (int q = lane; q < nw; q += 32) words[q] = word_transform(words[q], nbits);
+    __syncwarp();
     for (int h = 1; h < nw; h <<= 1) {
-        for (int p = threadIdx.x; p < nw / 2; p += BLOCK) {
+        for (int p = lane; p < nw / 2; p += 32) {
             const int q = ((p / h) * 2 * h) + (p % h);
             words[q] ^= words[q + h];
         }
-        __syncthreads();
+        __syncwarp();
     }
 }
 
@@ -90,7 +89,7 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
     uint8_t* fst = reinterpret_cast<uint8_t*>(smem + 4 * nw_all);  // freeze_stage per row
 
     __shared__ long long s_frame;
-    __shared__ int s_frontier, s_nev;
+    __shared__ int s_frontier, s_nev, s_conv;
     __shared__ unsigned long long s_act;
     __shared__ int s_bit_err;
 
@@ -199,6 +198,8 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
 
                 // ---- candidate_block / check_csfg / apply_freeze
                 //      (src/csfg_freeze.cpp:8-39,82-93,116-118) ----
+                // x_hat of the block gathered by the CTA, its transform and the
+                // frozen-row verdict by one warp, the commit by the CTA
                 const int frontier = s_frontier;
                 const int sz = n >> (s + 1);
                 const int index = frontier / sz;
@@ -210,17 +211,21 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
                     if (lane == 0) wb0[i >> 5] = w;
                 }
                 __syncthreads();
-                cta_transform<BLOCK>(wb0, sz);
-                int viol = 0;
-                if (sz >= 32) {
-                    for (int q = tid; q < nw; q += BLOCK)
-                        viol |= (wb0[q] & a.frozen_bits[(start >> 5) + q]) != 0u;
-                } else if (tid == 0) {
-                    const uint32_t fz = (a.frozen_bits[start >> 5] >> (start & 31)) & low_mask(sz);
-                    viol = (wb0[0] & fz) != 0u;
+                if (tid < 32) {
+                    warp_transform(wb0, sz, lane);
+                    bool viol = false;
+                    if (sz >= 32) {
+                        for (int q = lane; q < nw; q += 32)
+                            viol |= (wb0[q] & a.frozen_bits[(start >> 5) + q]) != 0u;
+                    } else if (lane == 0) {
+                        const uint32_t fz = (a.frozen_bits[start >> 5] >> (start & 31)) & low_mask(sz);
+                        viol = (wb0[0] & fz) != 0u;
+                    }
+                    const bool acc = !__any_sync(0xffffffffu, viol);
+                    if (lane == 0) s_conv = acc ? 1 : 0;
                 }
-                const bool accept = !__syncthreads_or(viol);
-                if (accept) {
+                __syncthreads();
+                if (s_conv) {
                     for (int i = tid; i < sz; i += BLOCK) {
                         const int r = start + i;
                         L[(size_t)s * n + r] = (R[r] < T(0)) ? -cap : cap;  // L(s+1)
@@ -233,6 +238,7 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
                         const uint32_t msk = low_mask(sz) << off;
                         dec_u[start >> 5] = (dec_u[start >> 5] & ~msk) | ((wb0[0] << off) & msk);
                     }
+                    __syncthreads();  // s_frontier / s_conv read above by every thread
                     if (tid == 0) {
                         if (a.events && s_nev < a.ev_cap) {
                             int* e = a.events + ((size_t)frame * a.ev_cap + s_nev) * 5;
@@ -266,10 +272,15 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
                 }
             }
             __syncthreads();
-            cta_transform<BLOCK>(wb0, n);
-            int diff = 0;
-            for (int q = tid; q < nw_all; q += BLOCK) diff |= (wb0[q] != wb1[q]);
-            const bool conv = !__syncthreads_or(diff);
+            if (tid < 32) {  // transform and compare by one warp
+                warp_transform(wb0, n, lane);
+                bool diff = false;
+                for (int q = lane; q < nw_all; q += 32) diff |= (wb0[q] != wb1[q]);
+                const bool c = !__any_sync(0xffffffffu, diff);
+                if (lane == 0) s_conv = c ? 1 : 0;
+            }
+            __syncthreads();
+            const bool conv = s_conv != 0;
             if (a.kind == 1 && conv) {
                 iters = t;
                 stop = 1;

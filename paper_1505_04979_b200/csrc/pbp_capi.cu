@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -195,12 +196,14 @@ int begin_call(pbp_ctx* ctx, int max_sets) {
 
 // Grid of the generic kernel: every frame when it decodes alone, the
 // re-routed frames (at most one per SM at a time) after the warp kernel;
-// bounded by 1 GiB of per-CTA scratch.
+// bounded by 4 GiB of per-CTA scratch.
 long long generic_grid(const pbp_ctx* ctx, long long frames, bool fast, int esz = 1) {
     const long long gfm = fast ? std::min<long long>(frames, ctx->sm_count) : frames;
     const long long stride = pbp::generic_scratch_elems(ctx->n, ctx->m) * esz;
-    long long grid = std::min<long long>(gfm, (long long)ctx->sm_count * 4);
-    const long long max_scratch_floats = 1ll << 28;  // 1 GiB
+    // latency-bound (one CTA per frame, barriers per stage): fill every SM
+    // (measured: 4 -> 8 CTAs/SM is +26 % at n = 4096, +23 % at 16384)
+    long long grid = std::min<long long>(gfm, (long long)ctx->sm_count * 8);
+    const long long max_scratch_floats = 1ll << 30;  // 4 GiB
     return std::max<long long>(1, std::min<long long>(grid, max_scratch_floats / stride));
 }
 
