@@ -101,6 +101,54 @@ def test_random_llrs_vs_oracle(ctx, n, kind):
         assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), f
 
 
+def _random_frozen(rng, n, k):
+    """A frozen set with the information rows anywhere (not a polar construction):
+    info rows at low indices, unfrozen rows 0..31, odd block patterns."""
+    fz = np.ones(n, np.uint8)
+    fz[rng.choice(n, size=k, replace=False)] = 0
+    return fz
+
+
+@pytest.mark.parametrize("n", [128, 256, 512, 1024])
+@pytest.mark.parametrize("kind", ["gmatrix", "csfg"])
+@pytest.mark.parametrize("rate", [0.25, 0.5, 0.875])
+def test_random_frozen_sets_vs_oracle(ctx, n, kind, rate):
+    """Random frozen sets and channel-like LLRs at several SNRs: the csfg walks (window,
+    re-covered rows, G-check filter preconditions) against the oracle, both kernels."""
+    rng = np.random.default_rng(int(7000 * rate) + n + len(kind))
+    k = max(1, int(n * rate))
+    fz = _random_frozen(rng, n, k)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    frames = 96
+    scale = rng.choice([1.0, 2.0, 4.0, 8.0], size=(frames, 1))
+    llr = (scale * (1.0 + rng.normal(0.0, 1.0, size=(frames, n)))).astype(np.float32)
+    exp = O.decode_batch(kind, fz, llr, 0.9375, 30, prec=32)
+    for generic in (False, True):
+        ctx.force_generic(generic)
+        try:
+            got = P.decode_batch(code, kind, llr, 0.9375, 30, ctx=ctx)
+        finally:
+            ctx.force_generic(False)
+        assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"]), generic
+        for f in ("iterations", "pe", "stop", "n_events"):
+            assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), (f, generic)
+
+
+@pytest.mark.parametrize("alpha,max_iter", [(0.5, 12), (1.0, 20), (0.75, 60)])
+def test_other_alpha_and_iteration_caps(ctx, alpha, max_iter):
+    n = 1024
+    fz = O.construct(n, n // 2, Z0)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    _, llr64 = O.trials(3, 0, 64, fz, 2.0, lib=O.C)
+    llr = llr64.astype(np.float32)
+    for kind in ("baseline", "gmatrix", "csfg"):
+        exp = O.decode_batch(kind, fz, llr, alpha, max_iter, prec=32)
+        got = P.decode_batch(code, kind, llr, alpha, max_iter, ctx=ctx)
+        assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"]), kind
+        for f in ("iterations", "pe", "stop", "n_events"):
+            assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), (kind, f)
+
+
 @pytest.mark.parametrize("n", [256, 1024])
 def test_clamp_and_nonfinite_frames_rerouted(ctx, n):
     """Frames the clamp-free fast path cannot take go to the generic kernel (clamps kept)."""
