@@ -461,7 +461,7 @@ struct Dec {
     // this lane's rows (bit j = row_of(j)); the rest happens in verdicts().
     template <int S>
     __device__ __forceinline__ void snapshot() {
-        sm->su[S][lane] = pack_all();
+        if constexpr (S < PL::SL - 1) sm->su[S][lane] = pack_all();
     }
 
     // For every stage S < SL: x_hat's polar transform inside every block (all
@@ -491,18 +491,21 @@ struct Dec {
             for (int gp = 0; gp < b; ++gp) v |= __shfl_xor_sync(kFull, v, 1 << gp);
         }
     }
+    // stages 0 .. SL-2; stage SL-1's block is one row-order word of R(SL),
+    // which is in X when the walk runs (walk_early)
+    static constexpr int NV = PL::SL - 1;
     template <int S>
-    __device__ __forceinline__ void verdicts_from(uint32_t (&u)[PL::SL], uint32_t (&v)[PL::SL]) {
+    __device__ __forceinline__ void verdicts_from(uint32_t (&u)[NV], uint32_t (&v)[NV]) {
         verdict_of<S>(u[S], v[S]);
-        if constexpr (S + 1 < PL::SL) verdicts_from<S + 1>(u, v);
+        if constexpr (S + 1 < NV) verdicts_from<S + 1>(u, v);
     }
     __device__ __forceinline__ void verdicts() {
-        uint32_t u[PL::SL], v[PL::SL];
+        uint32_t u[NV], v[NV];
 #pragma unroll
-        for (int S = 0; S < PL::SL; ++S) u[S] = sm->su[S][lane];
+        for (int S = 0; S < NV; ++S) u[S] = sm->su[S][lane];
         verdicts_from<0>(u, v);
 #pragma unroll
-        for (int S = 0; S < PL::SL; ++S) {
+        for (int S = 0; S < NV; ++S) {
             sm->sv[S][lane] = v[S];
             sm->su[S][lane] = u[S];
         }
@@ -526,10 +529,23 @@ struct Dec {
         s_last_ = M - 1;
         done_ = false;
         int s_next = 0;
+        constexpr int g4 = M - SL;  // stage SL-1: blocks of 2^g4 <= 32 rows
+        uint32_t u4 = 0u;
 #pragma unroll 1
         while (s_next < SL) {
+            // stage SL-1's candidate: its rows' sign bits straight from R(SL) in X
+            const int A4 = (frontier >> g4) << g4;
+            {
+                const float xv = sm->X[Q - 2][xpad((A4 & ~31) + lane)];
+                const uint32_t w4 = __ballot_sync(kFull, __float_as_int(xv) < 0);
+                u4 = (w4 >> (A4 & 31)) & low_mask(1 << g4);
+#pragma unroll
+                for (int tp = 0; tp < g4; ++tp) u4 ^= (u4 >> (1 << tp)) & jmask(tp);
+            }
             bool acc = false;
-            if (lane >= s_next && lane < SL) {
+            if (lane == SL - 1 && lane >= s_next) {
+                acc = (u4 & (sm->frz[A4 >> 5] >> (A4 & 31)) & low_mask(1 << g4)) == 0u;
+            } else if (lane >= s_next && lane < SL - 1) {
                 const int st = lane;
                 const int q = st / K;
                 const int b = (M - K - q * K) > 0 ? (M - K - q * K) : 0;
@@ -548,6 +564,15 @@ struct Dec {
             if (lane == 0) {
                 sm->cS[nc] = st;
                 sm->cbi[nc] = frontier >> g;
+            }
+            if (st == SL - 1) {
+                // u_hat of the block in the pass layout, for apply_commits:
+                // lane bit j0 = u of the row this lane holds at register j0
+                constexpr int qq = Q - 2, b = PL::base_bit(qq);
+                const int j0 = (A4 >> b) & (P - 1);
+                const int r = row_of<qq>(j0);
+                const bool in = r >= A4 && r < A4 + (1 << g4);
+                sm->su[SL - 1][lane] = in ? (((u4 >> (r - A4)) & 1u) << j0) : 0u;
             }
             ++nc;
             frontier = ((frontier >> g) + 1) << g;
