@@ -105,6 +105,7 @@ struct pbp_ctx {
     DevBuf<unsigned long long> rerouted;  // per launch of the last call: frames re-routed
     int n_launch_sets = 0;
     long long rerouted_host = -1;         // the last call's count when known on the host
+    int warp_occ[11][3] = {};             // resident warp-kernel CTAs per SM by (m, kind), 0 = not queried
     DevBuf<long long> blist;              // batch-wide re-route list (pipelined host batch)
     DevBuf<unsigned long long> bctl;      // [0] its length, [1] generic queue
     // host-API staging
@@ -194,6 +195,13 @@ int begin_call(pbp_ctx* ctx, int max_sets) {
     return ctx->rerouted.ensure((size_t)std::max(max_sets, 16));
 }
 
+// resident warp-kernel CTAs per SM (queried once per context and code length)
+int warp_occupancy(pbp_ctx* ctx, int kind) {
+    int& v = ctx->warp_occ[ctx->m][kind];
+    if (!v) v = std::max(1, pbp::warp_blocks_per_sm(ctx->m, kind));
+    return v;
+}
+
 // Grid of the generic kernel: every frame when it decodes alone, the
 // re-routed frames (at most one per SM at a time) after the warp kernel;
 // bounded by 4 GiB of per-CTA scratch.
@@ -213,7 +221,7 @@ int size_slot(pbp_ctx* ctx, DecodeSlot& s, int kind, long long frames) {
     int rc;
     if ((rc = s.ctl.ensure(4)) || (rc = s.list.ensure(std::max<long long>(frames, 1)))) return rc;
     if (pbp::warp_kernel_supported(ctx->m)) {
-        const int per_sm = std::max(1, pbp::warp_blocks_per_sm(ctx->m, kind));
+        const int per_sm = warp_occupancy(ctx, kind);
         const long long grid = std::min<long long>((long long)per_sm * ctx->sm_count, std::max<long long>(frames, 1));
         if ((rc = s.r0s.ensure((size_t)(grid * ctx->n)))) return rc;
     }
@@ -262,7 +270,7 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
         a.frame_base = r.frame_base;
         a.queue = s.ctl.p + 0;
         a.list_mode = 0;
-        const int per_sm = std::max(1, pbp::warp_blocks_per_sm(ctx->m, r.kind));
+        const int per_sm = warp_occupancy(ctx, r.kind);
         const long long grid = std::min<long long>((long long)per_sm * ctx->sm_count, r.frames);
         a.r0s = s.r0s.p;
         cudaError_t e = pbp::launch_warp(a, (int)grid, st);
@@ -571,14 +579,17 @@ int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
         return rc;
     // Chunks round-robin over the slots' streams: the host->device copy of one
     // chunk overlaps the decode of the others (and a decode's tail overlaps
-    // the next chunk's launch). A small first chunk starts the GPU early.
-    constexpr long long kChunkMin = 16384, kFirst = 4096;
+    // the next chunk's launch).
+    // Small first and last chunks: the GPU starts after a short copy and the
+    // last kernel's tail (frames still iterating) is short.
+    constexpr long long kChunkMin = 16384, kEdge = 4096;
     std::vector<long long> bounds{0};
     if (frames >= 2 * kChunkMin) {
-        bounds.push_back(kFirst);
-        const long long rest = frames - kFirst;
-        const long long nrest = std::min<long long>(7, rest / kChunkMin);
-        for (long long i = 1; i <= nrest; ++i) bounds.push_back(kFirst + rest * i / nrest);
+        bounds.push_back(kEdge);
+        const long long mid = frames - 2 * kEdge;
+        const long long nmid = std::max<long long>(1, std::min<long long>(6, mid / kChunkMin));
+        for (long long i = 1; i <= nmid; ++i) bounds.push_back(kEdge + mid * i / nmid);
+        bounds.push_back(frames);
     } else {
         bounds.push_back(frames);
     }
