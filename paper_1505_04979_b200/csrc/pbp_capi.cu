@@ -83,6 +83,7 @@ struct DevBuf {
 // scratch are per launch, so decodes on different streams need their own.
 struct DecodeSlot {
     cudaStream_t stream = nullptr;     // slot 0: the context stream
+    cudaEvent_t done = nullptr;        // after the slot's last use (any stream)
     DevBuf<unsigned long long> ctl;    // [0] warp queue, [1] generic queue, [2] list length
     DevBuf<long long> list;
     DevBuf<float> scratch;             // generic kernel: per-CTA message arrays
@@ -95,6 +96,7 @@ struct pbp_ctx {
     int sm_count = 0;
     cudaStream_t stream = nullptr;
     DecodeSlot slot[kSlots];
+    int next_slot = 0;  // device-pointer calls rotate over the slots
     // code tables
     std::vector<uint8_t> code_key;
     int n = 0, m = 0, k = 0;
@@ -195,6 +197,14 @@ int begin_call(pbp_ctx* ctx, int max_sets) {
     return ctx->rerouted.ensure((size_t)std::max(max_sets, 16));
 }
 
+// launch resources for an asynchronous device-pointer call: rotated, so
+// calls on different streams overlap; run_decode orders each slot's uses
+DecodeSlot& next_slot(pbp_ctx* ctx) {
+    DecodeSlot& s = ctx->slot[ctx->next_slot];
+    ctx->next_slot = (ctx->next_slot + 1) % kSlots;
+    return s;
+}
+
 // resident warp-kernel CTAs per SM (queried once per context and code length)
 int warp_occupancy(pbp_ctx* ctx, int kind) {
     int& v = ctx->warp_occ[ctx->m][kind];
@@ -238,6 +248,8 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
     if (r.frames == 0) return PBP_OK;
     int rc;
     if ((rc = size_slot(ctx, s, r.kind, r.frames))) return rc;
+    // the slot's queue/scratch may still be in use by a launch on another stream
+    PBP_CUDA(cudaStreamWaitEvent(st, s.done, 0));
     PBP_CUDA(cudaMemsetAsync(s.ctl.p, 0, 4 * sizeof(unsigned long long), st));
     pbp::DecodeArgs a{};
     a.n = ctx->n;
@@ -276,7 +288,10 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
         cudaError_t e = pbp::launch_warp(a, (int)grid, st);
         if (e != cudaSuccess) return cuda_fail(e, "bp_warp_kernel launch");
         ctx->last_launches += 1;
-        if (r.list) return PBP_OK;  // the caller runs the generic pass over the shared list
+        if (r.list) {  // the caller runs the generic pass over the shared list
+            PBP_CUDA(cudaEventRecord(s.done, st));
+            return PBP_OK;
+        }
         // frames the fast kernel re-routed (|LLR| beyond the clamp-free bound)
         a.list_mode = 1;
     } else {
@@ -301,6 +316,7 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
                                  cudaMemcpyDeviceToDevice, st));
         ctx->n_launch_sets += 1;
     }
+    PBP_CUDA(cudaEventRecord(s.done, st));
     return PBP_OK;
 }
 
@@ -309,6 +325,7 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
 int run_generic_list(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st, long long listed) {
     int rc;
     if ((rc = s.ctl.ensure(4))) return rc;
+    PBP_CUDA(cudaStreamWaitEvent(st, s.done, 0));
     PBP_CUDA(cudaMemsetAsync(s.ctl.p, 0, 4 * sizeof(unsigned long long), st));
     pbp::DecodeArgs a{};
     a.n = ctx->n;
@@ -343,6 +360,7 @@ int run_generic_list(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream
     cudaError_t e = pbp::launch_generic(a, (int)grid, st);
     if (e != cudaSuccess) return cuda_fail(e, "bp_generic_kernel launch");
     ctx->last_launches += 1;
+    PBP_CUDA(cudaEventRecord(s.done, st));
     return PBP_OK;
 }
 
@@ -409,6 +427,12 @@ int pbp_ctx_create(int device, pbp_ctx** out) {
         return cuda_fail(e, "cudaStreamCreate");
     }
     ctx->slot[0].stream = ctx->stream;
+    for (int i = 0; i < kSlots && e == cudaSuccess; ++i)
+        e = cudaEventCreateWithFlags(&ctx->slot[i].done, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        pbp_ctx_destroy(ctx);
+        return cuda_fail(e, "cudaEventCreate");
+    }
     *out = ctx;
     return PBP_OK;
 }
@@ -425,6 +449,7 @@ int pbp_ctx_destroy(pbp_ctx* ctx) {
             cudaStreamSynchronize(ctx->slot[i].stream);
             cudaStreamDestroy(ctx->slot[i].stream);
         }
+        if (ctx->slot[i].done) cudaEventDestroy(ctx->slot[i].done);
         ctx->slot[i].ctl.release();
         ctx->slot[i].list.release();
         ctx->slot[i].scratch.release();
@@ -562,7 +587,7 @@ int pbp_decode_batch_device(pbp_ctx* ctx, const pbp_code* code, int decoder, con
         r.nev = out_dev->n_events;
     }
     if ((rc = begin_call(ctx, 1))) return rc;
-    return run_decode(ctx, r, ctx->slot[0], pick(ctx, stream));
+    return run_decode(ctx, r, next_slot(ctx), pick(ctx, stream));
 }
 
 int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs,
@@ -783,7 +808,7 @@ int pbp_decode_batch_f64_device(pbp_ctx* ctx, const pbp_code* code, int decoder,
         r.nev = out_dev->n_events;
     }
     if ((rc = begin_call(ctx, 1))) return rc;
-    return run_decode(ctx, r, ctx->slot[0], pick(ctx, stream));
+    return run_decode(ctx, r, next_slot(ctx), pick(ctx, stream));
 }
 
 int pbp_decode_batch_f64(pbp_ctx* ctx, const pbp_code* code, int decoder, const double* llrs, int64_t frames,
@@ -888,7 +913,7 @@ int pbp_decode_count_device(pbp_ctx* ctx, const pbp_code* code, int decoder, con
     r.truth = u_dev;
     r.counters = reinterpret_cast<unsigned long long*>(counters_dev);
     if ((rc = begin_call(ctx, 1))) return rc;
-    return run_decode(ctx, r, ctx->slot[0], pick(ctx, stream));
+    return run_decode(ctx, r, next_slot(ctx), pick(ctx, stream));
 }
 
 // run_point's trial loop on the device: fp32 LLRs (the fast path) or, with

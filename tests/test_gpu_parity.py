@@ -293,3 +293,40 @@ def test_edge_cases(ctx):
             got = P.decode_batch(c, kind, l, 0.9375, 5, ctx=ctx)
             assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"]), (n, kind)
             assert np.array_equal(got["iterations"], exp["iterations"]), (n, kind)
+
+
+def test_concurrent_device_calls_on_two_streams(ctx):
+    """Device-pointer decodes queued on two streams of one context at once: each call gets
+    its own launch resources (rotated slots, ordered by events), results unchanged."""
+    import ctypes as C
+    import torch
+    n, frames = 1024, 20000
+    code = P.PolarCode.construct(n, n // 2, Z0)
+    cs = code.c_struct()
+    llr, _, _ = P.generate(code, 21, 0, 2 * frames, 2.5, ctx=ctx)
+    ref = P.decode_batch(code, "csfg", llr, 0.9375, 40, ctx=ctx)
+    dev = torch.device("cuda", 0)
+    d_llr = torch.from_numpy(llr).to(dev)
+    nw = n // 32
+    outs, streams = [], [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    torch.cuda.synchronize()
+    for i, st in enumerate(streams):
+        o = {"u": torch.empty((frames, nw), dtype=torch.int32, device=dev),
+             "it": torch.empty(frames, dtype=torch.int32, device=dev),
+             "pe": torch.empty(frames, dtype=torch.int64, device=dev),
+             "st": torch.empty(frames, dtype=torch.uint8, device=dev),
+             "ne": torch.empty(frames, dtype=torch.int32, device=dev)}
+        fo = P._abi.PbpFrameOut(P._abi.u32p(o["u"].data_ptr()), P._abi.i32p(o["it"].data_ptr()),
+                                P._abi.i64p(o["pe"].data_ptr()), P._abi.u8p(o["st"].data_ptr()),
+                                P._abi.i32p(o["ne"].data_ptr()))
+        part = d_llr[i * frames:(i + 1) * frames]
+        P._check(P.lib.pbp_decode_batch_device(ctx.handle, C.byref(cs), 2, P._abi.f32p(part.data_ptr()),
+                                               frames, 0.9375, 40, C.byref(fo), C.c_void_p(st.cuda_stream)))
+        outs.append(o)
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        sl = slice(i * frames, (i + 1) * frames)
+        assert np.array_equal(o["u"].cpu().numpy().view(np.uint32), ref["u_hat_bits"][sl])
+        assert np.array_equal(o["it"].cpu().numpy(), ref["iterations"][sl])
+        assert np.array_equal(o["pe"].cpu().numpy(), ref["pe"][sl])
+        assert np.array_equal(o["ne"].cpu().numpy(), ref["n_events"][sl])
