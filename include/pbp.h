@@ -60,7 +60,11 @@ typedef struct {
 
 /* One device context: device buffers, stream, cached code tables. Not
  * thread-safe; use one context per host thread (reference decoders are
- * pure functions, SPEC: concurrent calls on distinct frames are safe). */
+ * pure functions, SPEC: concurrent calls on distinct frames are safe).
+ * From one thread, asynchronous device-pointer calls may be queued on
+ * different streams of the same context: each call takes one of the
+ * context's launch-resource slots in turn, and a slot's next use waits for
+ * its previous one. */
 typedef struct pbp_ctx pbp_ctx;
 
 /* Per-frame outputs of a batch (DecodeOutcome, include/polarbp/bp_core.hpp:51-57
