@@ -247,7 +247,9 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
     if (r.frames < 0) return fail(PBP_EINVAL, "frames < 0");
     if (r.frames == 0) return PBP_OK;
     int rc;
-    if ((rc = size_slot(ctx, s, r.kind, r.frames))) return rc;
+    // every slot at once: a later growth (cudaFree) would stall the device
+    for (int i = 0; i < kSlots; ++i)
+        if ((rc = size_slot(ctx, ctx->slot[i], r.kind, r.frames))) return rc;
     // the slot's queue/scratch may still be in use by a launch on another stream
     PBP_CUDA(cudaStreamWaitEvent(st, s.done, 0));
     PBP_CUDA(cudaMemsetAsync(s.ctl.p, 0, 4 * sizeof(unsigned long long), st));
