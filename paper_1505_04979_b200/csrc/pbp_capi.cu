@@ -607,16 +607,26 @@ int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
     // Chunks round-robin over the slots' streams: the host->device copy of one
     // chunk overlaps the decode of the others (and a decode's tail overlaps
     // the next chunk's launch).
-    // Small first and last chunks: the GPU starts after a short copy and the
-    // last kernel's tail (frames still iterating) is short.
-    constexpr long long kChunkMin = 16384, kEdge = 4096;
+    // Chunk sizes double from 4096 frames up to 2^17 and halve again towards
+    // the end: a chunk's copy (PCIe is ~2x faster than the decode) hides
+    // under the previous chunk's decode, and the last kernel's tail is short.
+    constexpr long long kChunkMin = 16384, kEdge = 4096, kCap = 1 << 17;
     std::vector<long long> bounds{0};
     if (frames >= 2 * kChunkMin) {
-        bounds.push_back(kEdge);
-        const long long mid = frames - 2 * kEdge;
-        const long long nmid = std::max<long long>(1, std::min<long long>(6, mid / kChunkMin));
-        for (long long i = 1; i <= nmid; ++i) bounds.push_back(kEdge + mid * i / nmid);
-        bounds.push_back(frames);
+        std::vector<long long> head, tail;
+        long long rem = frames, sz = kEdge;
+        while (rem > 0) {
+            const long long a = std::min(sz, rem);
+            head.push_back(a);
+            rem -= a;
+            if (rem <= 0) break;
+            const long long b = std::min(sz, rem);
+            tail.push_back(b);
+            rem -= b;
+            sz = std::min(sz * 2, kCap);
+        }
+        for (long long v : head) bounds.push_back(bounds.back() + v);
+        for (auto it = tail.rbegin(); it != tail.rend(); ++it) bounds.push_back(bounds.back() + *it);
     } else {
         bounds.push_back(frames);
     }
