@@ -88,6 +88,10 @@ struct DecodeSlot {
     DevBuf<long long> list;
     DevBuf<float> scratch;             // generic kernel: per-CTA message arrays
     DevBuf<float> r0s;                 // warp kernel: per-CTA channel LLRs
+    // frames generated on the device by simulate_point (asynchronous calls)
+    DevBuf<float> gen_llr;
+    DevBuf<double> gen_llr64;
+    DevBuf<uint32_t> gen_truth;
 };
 constexpr int kSlots = 3;
 
@@ -113,7 +117,7 @@ struct pbp_ctx {
     // host-API staging
     DevBuf<float> llr;
     DevBuf<double> llr64;
-    DevBuf<uint32_t> ubits, truth;
+    DevBuf<uint32_t> ubits;
     DevBuf<int> iters, nev, events;
     DevBuf<long long> pe;
     DevBuf<uint8_t> stop;
@@ -456,6 +460,9 @@ int pbp_ctx_destroy(pbp_ctx* ctx) {
         ctx->slot[i].list.release();
         ctx->slot[i].scratch.release();
         ctx->slot[i].r0s.release();
+        ctx->slot[i].gen_llr.release();
+        ctx->slot[i].gen_llr64.release();
+        ctx->slot[i].gen_truth.release();
     }
     ctx->rerouted.release();
     ctx->blist.release();
@@ -464,7 +471,6 @@ int pbp_ctx_destroy(pbp_ctx* ctx) {
     ctx->counters.release();
     ctx->llr.release();
     ctx->ubits.release();
-    ctx->truth.release();
     ctx->iters.release();
     ctx->nev.release();
     ctx->events.release();
@@ -941,29 +947,33 @@ static int simulate_point_impl(pbp_ctx* ctx, const pbp_code* code, int decoder, 
     const int n = ctx->n, nw = (n + 31) / 32;
     // chunk so the staging stays bounded (~256 MiB of LLRs)
     const long long chunk = std::max<long long>(1, std::min<long long>(frames, (1ll << 26) / n));
-    if ((rc = ctx->llr.ensure((size_t)chunk * n)) || (rc = ctx->truth.ensure((size_t)chunk * nw))) return rc;
-    if (f64 && (rc = ctx->llr64.ensure((size_t)chunk * n))) return rc;
+    // this call's slot: its generation staging and launch resources (an
+    // asynchronous call may overlap other calls on other streams)
+    DecodeSlot& sl = next_slot(ctx);
+    if ((rc = sl.gen_llr.ensure((size_t)chunk * n)) || (rc = sl.gen_truth.ensure((size_t)chunk * nw))) return rc;
+    if (f64 && (rc = sl.gen_llr64.ensure((size_t)chunk * n))) return rc;
     cudaStream_t st = pick(ctx, stream);
     if ((rc = begin_call(ctx, (int)((frames + chunk - 1) / chunk)))) return rc;
     for (long long done = 0; done < frames; done += chunk) {
         const long long c = std::min(chunk, frames - done);
-        if ((rc = run_generate(ctx, seed, first_trial + done, c, ebn0_db, noiseless, ctx->llr.p,
-                               f64 ? ctx->llr64.p : nullptr, ctx->truth.p, st)))
+        PBP_CUDA(cudaStreamWaitEvent(st, sl.done, 0));  // the slot's previous decode read the staging
+        if ((rc = run_generate(ctx, seed, first_trial + done, c, ebn0_db, noiseless, sl.gen_llr.p,
+                               f64 ? sl.gen_llr64.p : nullptr, sl.gen_truth.p, st)))
             return rc;
         DecodeReq r;
         r.kind = decoder;
         if (f64) {
-            r.llr64 = ctx->llr64.p;
+            r.llr64 = sl.gen_llr64.p;
             r.alpha64 = alpha;
         } else {
-            r.llr = ctx->llr.p;
+            r.llr = sl.gen_llr.p;
             r.alpha = (float)alpha;
         }
         r.frames = c;
         r.max_iter = max_iter;
-        r.truth = ctx->truth.p;
+        r.truth = sl.gen_truth.p;
         r.counters = reinterpret_cast<unsigned long long*>(counters_dev);
-        if ((rc = run_decode(ctx, r, ctx->slot[0], st))) return rc;
+        if ((rc = run_decode(ctx, r, sl, st))) return rc;
     }
     return PBP_OK;
 }

@@ -330,3 +330,25 @@ def test_concurrent_device_calls_on_two_streams(ctx):
         assert np.array_equal(o["it"].cpu().numpy(), ref["iterations"][sl])
         assert np.array_equal(o["pe"].cpu().numpy(), ref["pe"][sl])
         assert np.array_equal(o["ne"].cpu().numpy(), ref["n_events"][sl])
+
+
+def test_concurrent_simulate_point_device(ctx):
+    """Two asynchronous simulate_point calls on two streams of one context (each generates
+    into its own slot's staging) give the counters of the calls run one after another."""
+    import ctypes as C
+    import torch
+    code = P.PolarCode.construct(1024, 512, Z0)
+    cs = code.c_struct()
+    exp = [P.simulate_point(code, "csfg", 2, a, 30000, e, ctx=ctx) for a, e in ((0, 2.0), (30000, 3.0))]
+    dev = torch.device("cuda", 0)
+    cnt = torch.zeros((2, 10), dtype=torch.int64, device=dev)
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    torch.cuda.synchronize()
+    for i, (st, (a, e)) in enumerate(zip(streams, ((0, 2.0), (30000, 3.0)))):
+        P._check(P.lib.pbp_simulate_point_device(ctx.handle, C.byref(cs), 2, C.c_uint64(2), a, 30000, e, 0,
+                                                 0.9375, 40, P._abi.i64p(cnt[i].data_ptr()),
+                                                 C.c_void_p(st.cuda_stream)))
+    torch.cuda.synchronize()
+    got = cnt.cpu().numpy()
+    for i in range(2):
+        assert [int(x) for x in got[i]] == [exp[i][k] for k in P.COUNTER_FIELDS], i
