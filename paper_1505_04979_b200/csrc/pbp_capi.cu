@@ -145,6 +145,8 @@ int upload_code(pbp_ctx* ctx, const pbp_code* code) {
     if (rc) return rc;
     std::vector<uint8_t> key(code->frozen, code->frozen + code->n);
     if (ctx->n == code->n && key == ctx->code_key) return PBP_OK;
+    // asynchronous decodes of the previous code (any stream) still read the tables
+    PBP_CUDA(cudaDeviceSynchronize());
     const int n = code->n, nw = (n + 31) / 32;
     std::vector<uint32_t> bits(nw, 0u);
     std::vector<uint8_t> rows(n);
@@ -485,7 +487,7 @@ void* pbp_ctx_stream(pbp_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; 
 
 int pbp_ctx_synchronize(pbp_ctx* ctx) {
     if (!ctx) return fail(PBP_EINVAL, "null context");
-    PBP_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < kSlots; ++i) PBP_CUDA(cudaStreamSynchronize(ctx->slot[i].stream));
     return PBP_OK;
 }
 
