@@ -356,6 +356,10 @@ struct Dec {
         constexpr bool packed = true;
 #endif
         if constexpr (d >= 2 && packed) {
+            // stage 0: x_hat bits pushed into four independent 8-bit chains
+            // (pushes 8c..8c+7 in chain c), concatenated below into the same bit
+            // positions a single chain would give (push p at bit P-1-p)
+            uint32_t xqc[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
             for (int j = 0; j < P; j += 2) {
                 if (j & d) continue;
@@ -377,10 +381,11 @@ struct Dec {
                     float x0, x1, x2, x3;
                     add2(x0, x1, rt0, rt1, lt0o, lt1o);
                     add2(x2, x3, rb0, rb1, lb0o, lb1o);
-                    xq = __funnelshift_l(__float_as_uint(x0), xq, 1);
-                    xq = __funnelshift_l(__float_as_uint(x1), xq, 1);
-                    xq = __funnelshift_l(__float_as_uint(x2), xq, 1);
-                    xq = __funnelshift_l(__float_as_uint(x3), xq, 1);
+                    uint32_t& c = xqc[j >> 2];
+                    c = __funnelshift_l(__float_as_uint(x0), c, 1);
+                    c = __funnelshift_l(__float_as_uint(x1), c, 1);
+                    c = __funnelshift_l(__float_as_uint(x2), c, 1);
+                    c = __funnelshift_l(__float_as_uint(x3), c, 1);
                 }
                 Lt[j] = lt0o;
                 Lt[j + 1] = lt1o;
@@ -390,6 +395,15 @@ struct Dec {
                 R[j + 1] = rt1o;
                 R[j + d] = rb0o;
                 R[j + d + 1] = rb1o;
+            }
+            if constexpr (S == 0 && KIND != 0) {
+                uint32_t x = 0u;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int n = (P - 8 * c) < 8 ? (P - 8 * c) : 8;  // pushes in chain c
+                    if (n > 0) x |= xqc[c] << (P - 8 * c - n);
+                }
+                xq = x;
             }
         } else {
 #pragma unroll
