@@ -153,43 +153,57 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
                 if (s == 0 && n < 64)
                     for (int q = tid; q < nw_all; q += BLOCK) xh[q] = 0u;
                 if (s == 0) __syncthreads();
-                for (int p0 = 0; p0 < n / 2; p0 += BLOCK) {
-                    const int p = p0 + tid;
-                    bool xt = false, xbot = false;
-                    int r = 0;
-                    if (p < n / 2) {
-                        r = ((p >> ld) << (ld + 1)) | (p & (d - 1));
+                // two PEs per thread per step, all eight loads issued before the math
+                // (the messages sit in L2: one PE at a time leaves the loads' latency bare)
+                for (int p0 = 0; p0 < n / 2; p0 += 2 * BLOCK) {
+                    int r[2];
+                    bool on[2];
+                    T lt[2], lb[2], rt[2], rb[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int p = p0 + h * BLOCK + tid;
+                        r[h] = ((p >> ld) << (ld + 1)) | (p & (d - 1));
                         // is_pe_active (csfg_freeze.cpp:95-97); stage 0 is always active
-                        if (!(csfg && (int)fst[r] < s)) {
-                            const T lt = Ls1[r], lb = Ls1[r + d];
-                            const T rt = (s == 0) ? R0(r) : R[r], rb = (s == 0) ? R0(r + d) : R[r + d];
-                            const T cross = ref_f(alpha, lt, rt);
-                            const T sum_bot = O::add(lb, rb);
-                            const T l_top = ref_clamp(ref_f(alpha, lt, sum_bot));
-                            const T l_bot = ref_clamp(O::add(lb, cross));
-                            if (s > 0) {
-                                Ls[r] = l_top;
-                                Ls[r + d] = l_bot;
-                            } else {  // L(0) only feeds the G-check's x_hat (bp_core.cpp:99)
-                                xt = O::add(rt, l_top) < T(0);
-                                xbot = O::add(rb, l_bot) < T(0);
-                            }
-                            R[r] = ref_clamp(ref_f(alpha, rt, sum_bot));
-                            R[r + d] = ref_clamp(O::add(rb, cross));
-                            ++act;
+                        on[h] = p < n / 2 && !(csfg && (int)fst[r[h]] < s);
+                        if (on[h]) {
+                            lt[h] = Ls1[r[h]];
+                            lb[h] = Ls1[r[h] + d];
+                            rt[h] = (s == 0) ? R0(r[h]) : R[r[h]];
+                            rb[h] = (s == 0) ? R0(r[h] + d) : R[r[h] + d];
                         }
                     }
-                    if (s == 0) {
-                        if (n >= 64) {  // rows r = p and r + n/2: whole warps of consecutive rows
-                            const uint32_t wt = __ballot_sync(0xffffffffu, xt);
-                            const uint32_t wbt = __ballot_sync(0xffffffffu, xbot);
-                            if (lane == 0 && p < n / 2) {
-                                xh[r >> 5] = wt;
-                                xh[(r + d) >> 5] = wbt;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int p = p0 + h * BLOCK + tid;
+                        bool xt = false, xbot = false;
+                        if (on[h]) {
+                            const T cross = ref_f(alpha, lt[h], rt[h]);
+                            const T sum_bot = O::add(lb[h], rb[h]);
+                            const T l_top = ref_clamp(ref_f(alpha, lt[h], sum_bot));
+                            const T l_bot = ref_clamp(O::add(lb[h], cross));
+                            if (s > 0) {
+                                Ls[r[h]] = l_top;
+                                Ls[r[h] + d] = l_bot;
+                            } else {  // L(0) only feeds the G-check's x_hat (bp_core.cpp:99)
+                                xt = O::add(rt[h], l_top) < T(0);
+                                xbot = O::add(rb[h], l_bot) < T(0);
                             }
-                        } else if (p < n / 2) {
-                            if (xt) atomicOr(&xh[r >> 5], 1u << (r & 31));
-                            if (xbot) atomicOr(&xh[(r + d) >> 5], 1u << ((r + d) & 31));
+                            R[r[h]] = ref_clamp(ref_f(alpha, rt[h], sum_bot));
+                            R[r[h] + d] = ref_clamp(O::add(rb[h], cross));
+                            ++act;
+                        }
+                        if (s == 0) {
+                            if (n >= 64) {  // rows r = p and r + n/2: whole warps of consecutive rows
+                                const uint32_t wt = __ballot_sync(0xffffffffu, xt);
+                                const uint32_t wbt = __ballot_sync(0xffffffffu, xbot);
+                                if (lane == 0 && p < n / 2) {
+                                    xh[r[h] >> 5] = wt;
+                                    xh[(r[h] + d) >> 5] = wbt;
+                                }
+                            } else if (p < n / 2) {
+                                if (xt) atomicOr(&xh[r[h] >> 5], 1u << (r[h] & 31));
+                                if (xbot) atomicOr(&xh[(r[h] + d) >> 5], 1u << ((r[h] + d) & 31));
+                            }
                         }
                     }
                 }
