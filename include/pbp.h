@@ -187,8 +187,9 @@ int pbp_decode_count_device(pbp_ctx* ctx, const pbp_code* code, int decoder,
                             const float* llrs_dev, const uint32_t* u_dev, int64_t frames,
                             float alpha, int32_t max_iter, int64_t* counters_dev, void* stream);
 
-/* Which kernel serves a code length: 1 = warp-resident fast path,
- * 0 = CTA generic path. For tests and bench introspection. */
+/* Which kernel serves a code length: 1 = warp-resident fast path
+ * (n = 128..1024), 2 = CTA-per-frame register-pass path (n = 2048..16384),
+ * 0 = the generic kernel only. For tests and bench introspection. */
 int pbp_kernel_path(int32_t n);
 /* Route every decode of this context through the generic kernel (on != 0).
  * Test hook: lets the suite check both kernels against the oracle. */

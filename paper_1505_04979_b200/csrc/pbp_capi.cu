@@ -25,6 +25,10 @@ cudaError_t launch_warp(const DecodeArgs& a, int grid, cudaStream_t st);
 int warp_kernel_supported(int m);
 int warp_blocks_per_sm(int m, int kind);
 size_t warp_smem_bytes(int m);
+int cta_kernel_supported(int m);
+long long cta_scratch_floats(int m);
+cudaError_t launch_cta(const DecodeArgs& a, int grid, cudaStream_t st);
+int cta_blocks_per_sm(int m, int kind);
 cudaError_t launch_channel(const GenArgs& g, int grid, cudaStream_t stream);
 }  // namespace pbp
 
@@ -111,7 +115,7 @@ struct pbp_ctx {
     DevBuf<unsigned long long> rerouted;  // per launch of the last call: frames re-routed
     int n_launch_sets = 0;
     long long rerouted_host = -1;         // the last call's count when known on the host
-    int warp_occ[11][3] = {};             // resident warp-kernel CTAs per SM by (m, kind), 0 = not queried
+    int warp_occ[15][3] = {};             // resident fast-kernel CTAs per SM by (m, kind), 0 = not queried
     DevBuf<long long> blist;              // batch-wide re-route list (pipelined host batch)
     DevBuf<unsigned long long> bctl;      // [0] its length, [1] generic queue
     // host-API staging
@@ -211,10 +215,18 @@ DecodeSlot& next_slot(pbp_ctx* ctx) {
     return s;
 }
 
-// resident warp-kernel CTAs per SM (queried once per context and code length)
+// fast kernel for code length 2^m: 1 = warp-resident (n = 128..1024),
+// 2 = CTA per frame with register passes (n = 2048..16384), 0 = none
+int fast_kernel(int m) {
+    return pbp::warp_kernel_supported(m) ? 1 : (pbp::cta_kernel_supported(m) ? 2 : 0);
+}
+
+// resident fast-kernel CTAs per SM (queried once per context and code length)
 int warp_occupancy(pbp_ctx* ctx, int kind) {
     int& v = ctx->warp_occ[ctx->m][kind];
-    if (!v) v = std::max(1, pbp::warp_blocks_per_sm(ctx->m, kind));
+    if (!v)
+        v = std::max(1, fast_kernel(ctx->m) == 1 ? pbp::warp_blocks_per_sm(ctx->m, kind)
+                                                 : pbp::cta_blocks_per_sm(ctx->m, kind));
     return v;
 }
 
@@ -236,14 +248,20 @@ long long generic_grid(const pbp_ctx* ctx, long long frames, bool fast, int esz 
 int size_slot(pbp_ctx* ctx, DecodeSlot& s, int kind, long long frames) {
     int rc;
     if ((rc = s.ctl.ensure(4)) || (rc = s.list.ensure(std::max<long long>(frames, 1)))) return rc;
-    if (pbp::warp_kernel_supported(ctx->m)) {
+    size_t scratch = 0;
+    if (fast_kernel(ctx->m)) {
         const int per_sm = warp_occupancy(ctx, kind);
         const long long grid = std::min<long long>((long long)per_sm * ctx->sm_count, std::max<long long>(frames, 1));
-        if ((rc = s.r0s.ensure((size_t)(grid * ctx->n)))) return rc;
+        if (fast_kernel(ctx->m) == 1) {
+            if ((rc = s.r0s.ensure((size_t)(grid * ctx->n)))) return rc;
+        } else {
+            scratch = (size_t)(grid * pbp::cta_scratch_floats(ctx->m));
+        }
     }
-    const bool fast = !ctx->force_generic && pbp::warp_kernel_supported(ctx->m);
-    if (pbp::generic_in_smem(ctx->n, ctx->m, false)) return PBP_OK;
-    return s.scratch.ensure((size_t)generic_grid(ctx, frames, fast) * pbp::generic_scratch_elems(ctx->n, ctx->m));
+    const bool fast = !ctx->force_generic && fast_kernel(ctx->m);
+    if (!pbp::generic_in_smem(ctx->n, ctx->m, false))
+        scratch = std::max(scratch, (size_t)(generic_grid(ctx, frames, fast) * pbp::generic_scratch_elems(ctx->n, ctx->m)));
+    return scratch ? s.scratch.ensure(scratch) : PBP_OK;
 }
 
 // Launch the decode of `frames` frames already on the device, with slot s's
@@ -283,7 +301,8 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
     a.list_len = s.ctl.p + 2;
 
     // the warp kernel is fp32 only; fp64 decodes run the generic kernel on double
-    const bool fast = !r.llr64 && !r.force_generic && !ctx->force_generic && pbp::warp_kernel_supported(ctx->m);
+    const int fk = fast_kernel(ctx->m);
+    const bool fast = !r.llr64 && !r.force_generic && !ctx->force_generic && fk != 0;
     if (fast) {
         a.list = r.list ? r.list : s.list.p;
         if (r.list_len) a.list_len = r.list_len;
@@ -292,9 +311,16 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
         a.list_mode = 0;
         const int per_sm = warp_occupancy(ctx, r.kind);
         const long long grid = std::min<long long>((long long)per_sm * ctx->sm_count, r.frames);
-        a.r0s = s.r0s.p;
-        cudaError_t e = pbp::launch_warp(a, (int)grid, st);
-        if (e != cudaSuccess) return cuda_fail(e, "bp_warp_kernel launch");
+        cudaError_t e;
+        if (fk == 1) {
+            a.r0s = s.r0s.p;
+            e = pbp::launch_warp(a, (int)grid, st);
+        } else {
+            a.scratch = s.scratch.p;
+            a.scratch_stride = pbp::cta_scratch_floats(ctx->m);
+            e = pbp::launch_cta(a, (int)grid, st);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, fk == 1 ? "bp_warp_kernel launch" : "bp_cta_kernel launch");
         ctx->last_launches += 1;
         if (r.list) {  // the caller runs the generic pass over the shared list
             PBP_CUDA(cudaEventRecord(s.done, st));
@@ -505,7 +531,7 @@ int pbp_ctx_force_generic(pbp_ctx* ctx, int on) {
     return PBP_OK;
 }
 
-int pbp_kernel_path(int32_t n) { return is_pow2(n) && pbp::warp_kernel_supported(log2i(n)) ? 1 : 0; }
+int pbp_kernel_path(int32_t n) { return is_pow2(n) ? fast_kernel(log2i(n)) : 0; }
 
 int pbp_last_launch_info(pbp_ctx* ctx, int32_t* launches, int64_t* rerouted) {
     if (!ctx) return fail(PBP_EINVAL, "null context");
@@ -647,7 +673,7 @@ int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
     // frames re-routed by any chunk's fast kernel: one batch-wide list, decoded
     // by a single generic pass once the pipeline has drained (rare; no generic
     // launch between the chunks, whose CTAs would stall the other streams)
-    const bool fast = !ctx->force_generic && pbp::warp_kernel_supported(ctx->m);
+    const bool fast = !ctx->force_generic && fast_kernel(ctx->m) != 0;
     if (fast) {
         if ((rc = ctx->blist.ensure(std::max<long long>(frames, 1))) || (rc = ctx->bctl.ensure(2))) return rc;
         PBP_CUDA(cudaMemsetAsync(ctx->bctl.p, 0, 2 * sizeof(unsigned long long), ctx->stream));

@@ -33,7 +33,8 @@ def test_library_exports_every_declared_symbol():
 def test_version_and_paths():
     assert P.lib.pbp_version() == 1
     assert P.lib.pbp_kernel_path(1024) == 1 and P.lib.pbp_kernel_path(128) == 1
-    assert P.lib.pbp_kernel_path(4096) == 0 and P.lib.pbp_kernel_path(64) == 0
+    assert P.lib.pbp_kernel_path(4096) == 2 and P.lib.pbp_kernel_path(16384) == 2
+    assert P.lib.pbp_kernel_path(64) == 0 and P.lib.pbp_kernel_path(32768) == 0
 
 
 @pytest.mark.parametrize("n,k,z", [(2, 1, 0.5), (8, 4, 0.5), (64, 32, 0.5), (1024, 512, math.exp(-0.5)),

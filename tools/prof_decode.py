@@ -11,8 +11,11 @@ ap.add_argument("--ebn0", type=float, default=3.0)
 ap.add_argument("--kind", default="csfg")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--n", type=int, default=1024)
+ap.add_argument("--generic", action="store_true", help="force the generic kernel")
 a = ap.parse_args()
 ctx = P.Context(0)
+if a.generic:
+    ctx.force_generic(True)
 code = P.PolarCode.construct(a.n, a.n // 2, math.exp(-0.5))
 cs = code.c_struct()
 nw = max(1, a.n // 32)
