@@ -352,3 +352,42 @@ def test_concurrent_simulate_point_device(ctx):
     got = cnt.cpu().numpy()
     for i in range(2):
         assert [int(x) for x in got[i]] == [exp[i][k] for k in P.COUNTER_FIELDS], i
+
+
+@pytest.mark.parametrize("n", [2048, 4096, 8192])
+@pytest.mark.parametrize("kind", ["baseline", "gmatrix", "csfg"])
+def test_cta_kernel_vs_oracle(ctx, n, kind):
+    """n = 2048..16384 run on the CTA-per-frame register-pass kernel (pbp_kernel_path 2)."""
+    assert P.lib.pbp_kernel_path(n) == 2
+    fz = O.construct(n, n // 2, Z0)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    _, llr64 = O.trials(4, 0, 8 if n <= 4096 else 4, fz, 2.5, lib=O.C)
+    llr = llr64.astype(np.float32)
+    exp = O.decode_batch(kind, fz, llr, 0.9375, 30, prec=32)
+    got = P.decode_batch(code, kind, llr, 0.9375, 30, ctx=ctx)
+    assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"])
+    for f in ("iterations", "pe", "stop", "n_events"):
+        assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), f
+
+
+def test_cta_kernel_reroute_and_events(ctx):
+    n = 4096
+    fz = O.construct(n, n // 2, Z0)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    _, llr64 = O.trials(4, 0, 6, fz, 2.5, lib=O.C)
+    llr = llr64.astype(np.float32)
+    llr[1, 5] = 1e30          # re-routed to the generic kernel (clamps kept)
+    llr[4, :] *= 1e25
+    exp = O.decode_batch("csfg", fz, llr, 0.9375, 40, prec=32)
+    got = P.decode_batch(code, "csfg", llr, 0.9375, 40, ctx=ctx)
+    assert ctx.last_launch_info()[1] == 2
+    assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"])
+    for f in ("iterations", "pe", "stop", "n_events"):
+        assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), f
+    for i in (0, 2):
+        events = []
+        out = P.decode_csfg(code, llr[i], 0.9375, 40, events=events, ctx=ctx)
+        e = O.decode("csfg", fz, llr[i], 0.9375, 40, prec=32)
+        got_ev = np.array([[x.iteration, x.stage, x.block, x.start, x.size] for x in events], np.int64)
+        assert np.array_equal(got_ev.reshape(-1, 5), np.asarray(e["events"], np.int64).reshape(-1, 5)), i
+        assert out.pe_activations == e["pe"] and out.iterations_used == e["iterations"], i
