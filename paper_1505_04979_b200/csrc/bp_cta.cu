@@ -1,45 +1,112 @@
 // CTA-per-frame BP decoder for n = 2048 .. 16384 (configs 3 and 4).
 //
 // The reference schedule literally (src/bp_core.cpp:58-86, csfg_freeze.cpp:
-// 99-152): every stage's PEs, the PE mask of is_pe_active (inactive PEs are
-// skipped, so frozen boundaries keep their saturation without protection),
-// the candidate check/commit right after each stage and the pinned G-check
-// after each sweep. What changes is where the messages live: T = 512 (1024
-// from n = 8192) threads own P = n/T rows each, and for the K = log2 P stages of a pass a thread's rows
-// stay fixed, so R(s) is carried in registers from stage to stage and only
-// crosses shared memory at the pass boundaries. Each PE then moves 16 bytes of
-// messages (L(s+1) in, L(s) out; per-CTA global scratch, L2-resident at
-// n = 4096) instead of 32. Arithmetic as in the warp-resident kernel (one
-// min.xorsign.abs per min-with-sign, every product and sum rounded on its own,
-// r_top = fma(alpha, m, +0)); frames with |LLR| beyond the clamp-free bound or
-// non-finite are re-routed to the generic kernel, which keeps every clamp.
+// 99-152): every stage's PEs under the is_pe_active mask (inactive PEs are
+// skipped), the candidate check/commit right after each stage and the pinned
+// G-check after each sweep. What is B200-specific is where the state lives:
+//
+// * T threads own P = n/T rows each. A pass is K = log2 P consecutive stages
+//   whose PE distances are register bits of the thread's rows, so R(s) is
+//   carried in registers from stage to stage and crosses shared memory
+//   (Rx) only between passes.
+// * L(s) for a stage s inside a pass is produced and consumed by the same
+//   thread (stage s writes it, stage s-1 reads it, both in the pass's row
+//   layout): those levels live in registers. Levels at pass boundaries are
+//   exchanged between layouts in shared memory (or L2 for n >= 8192, where
+//   shared memory runs out); L(m) in {0, +-CAP} is two bit masks.
+// * The candidate check (polar transform of the block's hard decisions,
+//   csfg_freeze.cpp:18-39) and the G-check transform run where the bits are:
+//   the row bits held in a thread's registers in-thread, lane bits by
+//   shuffles, warp bits by one shared-memory superset XOR, and the verdict by
+//   __syncthreads_or: one or two barriers per stage. A commit
+//   (apply_freeze, csfg_freeze.cpp:82-93) is applied by the owners of the
+//   block's rows; frontier and event count are kept uniformly in registers.
+//
+// Arithmetic as in the warp-resident kernel (one min.xorsign.abs per
+// min-with-sign, every product and sum rounded on its own, r_top =
+// fma(alpha, m, +0) so R is never -0); frames with |LLR| beyond the
+// clamp-free bound or non-finite are re-routed to the generic kernel, which
+// keeps every clamp.
+#include <algorithm>
+#include <type_traits>
+
 #include "pbp_common.cuh"
 
 namespace pbp {
 namespace cta {
 
 constexpr unsigned kFull = 0xffffffffu;
+enum : int { kReg = 0, kSmem = 1, kGlob = 2, kBits = 3 };
 
-// threads per frame: 512 up to n = 4096 (two frames per SM at <= 64
-// registers), 1024 beyond (one frame per SM, 32 warps, scratch in HBM)
+// Per-size plan: threads (LOGT), rows per thread (2^K), where each L level
+// lives, whether R(0) stays in registers, whether Rx is double-buffered.
 template <int M>
-constexpr int kLogT = M <= 12 ? 9 : 10;
+struct Cfg;
+template <>
+struct Cfg<11> {  // 512 threads x 4 rows, 2 CTAs per SM
+    static constexpr int LOGT = 9, K = 2, MINB = 2;
+    static constexpr bool r0reg = true, rx2 = true;
+    static constexpr int where(int s) { return s == 11 ? kBits : (s & 1) ? kReg : kSmem; }
+};
+#ifndef PBP_CTA12_T1024
+template <>
+struct Cfg<12> {  // 512 x 8: four inner levels in registers, the other levels in shared memory
+    static constexpr int LOGT = 9, K = 3, MINB = 1;
+    static constexpr bool r0reg = true, rx2 = true;
+    static constexpr int where(int s) {
+        return s == 12 ? kBits : (s == 1 || s == 2 || s == 4 || s == 5) ? kReg : kSmem;
+    }
+};
+#else
+template <>
+struct Cfg<12> {  // 1024 x 4: inner levels (odd s) in registers, boundary levels in shared memory
+    static constexpr int LOGT = 10, K = 2, MINB = 1;
+    static constexpr bool r0reg = true, rx2 = true;
+    static constexpr int where(int s) { return s == 12 ? kBits : (s & 1) ? kReg : kSmem; }
+};
+#endif
+template <>
+struct Cfg<13> {  // 1024 x 8: boundary levels in shared memory, two in registers, the rest in L2
+    static constexpr int LOGT = 10, K = 3, MINB = 1;
+    static constexpr bool r0reg = false, rx2 = true;
+    static constexpr int where(int s) {
+        return s == 13 ? kBits : (s % 3 == 0) ? kSmem : (s <= 2) ? kReg : kGlob;
+    }
+};
+template <>
+struct Cfg<14> {  // 1024 x 16: one level in shared memory, the rest in L2
+    static constexpr int LOGT = 10, K = 4, MINB = 1;
+    static constexpr bool r0reg = false, rx2 = false;
+    static constexpr int where(int s) { return s == 14 ? kBits : (s == 4) ? kSmem : kGlob; }
+};
 
 template <int M_>
-struct CPlan {
+struct Plan {
+    using C = Cfg<M_>;
     static constexpr int M = M_;
     static constexpr int N = 1 << M;
-    static constexpr int T = 1 << kLogT<M>;
-    static constexpr int K = M - kLogT<M>;  // log2 of the rows per thread
+    static constexpr int LOGT = C::LOGT;
+    static constexpr int T = 1 << LOGT;
+    static constexpr int NWARP = T / 32;
+    static constexpr int K = C::K;
     static constexpr int P = 1 << K;
-    static constexpr int Q = (M + K - 1) / K;  // passes
+    static constexpr int Q = (M + K - 1) / K;
     static constexpr int NW = N / 32;
-    // pass q: registers j hold row bits [b, b+K); thread bits fill the rest
+    static_assert(K + LOGT == M, "rows per thread x threads = n");
+    static_assert(P <= 16, "a thread's rows are a sub-word group");
+    static_assert(M - K >= 5, "pass 0 keeps row bits [0, 5) in the lane index");
+    // pass q: register j holds row bits [b, b+K); thread bits fill the rest
     static constexpr int base(int q) { return (M - K * (q + 1)) > 0 ? (M - K * (q + 1)) : 0; }
-    static constexpr int first(int q) { return q * K; }
     static constexpr int last(int q) { return ((q + 1) * K < M ? (q + 1) * K : M) - 1; }
     static constexpr int pass_of(int s) { return s / K; }
-    static constexpr int pad(int row) { return row + (row >> 5); }  // bank spread of the transpose buffer
+    static constexpr int count(int kind, int below) {
+        int c = 0;
+        for (int s = 1; s < below; ++s) c += C::where(s) == kind;
+        return c;
+    }
+    static constexpr int slot(int s) { return count(C::where(s), s); }
+    static constexpr int NREG = count(kReg, M + 1), NSM = count(kSmem, M + 1), NGL = count(kGlob, M + 1);
+    static constexpr int pad(int row) { return row + (row >> 5); }
     static constexpr int NX = N + N / 32;
 };
 
@@ -49,48 +116,54 @@ __device__ __forceinline__ float xsmin(float a, float b) {
     return d;
 }
 
-// Polar transform (polar_code.cpp:13-20) of nbits bits in words[] by one warp.
-__device__ void warp_transform(uint32_t* words, int nbits, int lane) {
-    const int nw = (nbits + 31) >> 5;
-    for (int q = lane; q < nw; q += 32) words[q] = word_transform(words[q], nbits);
-    __syncwarp();
-    for (int h = 1; h < nw; h <<= 1) {
-        for (int p = lane; p < nw / 2; p += 32) {
-            const int q = ((p / h) * 2 * h) + (p % h);
-            words[q] ^= words[q + h];
-        }
-        __syncwarp();
-    }
+// bit i (i & h == 0) absorbs bit i + h for h < 2^NB: the in-thread levels of
+// the polar transform (polar_code.cpp:13-20) over a thread's register rows
+template <int NB>
+__device__ __forceinline__ uint32_t bits_transform(uint32_t w) {
+    if constexpr (NB > 0) w ^= (w >> 1) & 0x5555u;
+    if constexpr (NB > 1) w ^= (w >> 2) & 0x3333u;
+    if constexpr (NB > 2) w ^= (w >> 4) & 0x0F0Fu;
+    if constexpr (NB > 3) w ^= (w >> 8) & 0x00FFu;
+    return w;
 }
 
 template <int M>
-struct CtaSmem {
-    using PL = CPlan<M>;
-    float Rx[PL::NX];           // R at pass boundaries, row-indexed (padded)
-    uint8_t sgn[PL::N];         // sign of R(s+1) per row, for the candidate check
-    uint8_t fst[PL::N];         // freeze_stage per row
-    uint32_t xh[PL::NW];        // x_hat = (R(0) + L(0) < 0) of the last sweep
-    uint32_t dec_u[PL::NW];     // decided_u
-    uint32_t wb0[PL::NW];       // block / u_hat words
-    uint32_t frz[PL::NW];       // frozen rows
+struct Smem {
+    using PL = Plan<M>;
+    float Ls[PL::NSM > 0 ? PL::NSM : 1][PL::NX];  // shared-memory L levels, row-indexed (padded)
+    float Rx[Cfg<M>::rx2 ? 2 : 1][PL::NX];         // R at pass boundaries
+    typename std::conditional<(PL::Q * PL::P > 32), unsigned long long, uint32_t>::type buf[PL::T];  // cross-warp words
+    uint32_t vw[3];                                // verdict words of the pass checks
+    uint32_t dec[PL::NW];                          // decided_u
+    uint32_t xh[PL::NW];                           // x_hat = (R(0) + L(0) < 0) of the last sweep
+    uint8_t fst[PL::N];                            // freeze_stage per row
     long long frame;
-    unsigned long long act;
-    int frontier, nev, conv, accept, bad, bit_err;
 };
 
 template <int M, int KIND>
 struct Dec {
-    using PL = CPlan<M>;
+    using PL = Plan<M>;
+    using C = Cfg<M>;
     static constexpr int N = PL::N, P = PL::P, K = PL::K, Q = PL::Q, NW = PL::NW, kT = PL::T;
     static constexpr bool csfg = KIND == 2;
 
-    CtaSmem<M>* sm;
+    Smem<M>* sm;
     const DecodeArgs* a;
-    float* L;  // L(s) at L + (s-1) N, s = 1..M
-    int tid, lane;
+    float* Lg;  // L2 levels, N floats each
+    const float* llr;
+    int tid, lane, warp;
     float alpha;
     float R[P];
-    long long act;  // this thread's PE activations
+    float R0[C::r0reg ? P : 1];
+    float Lr[PL::NREG > 0 ? PL::NREG : 1][P];
+    uint32_t lm_nz, lm_neg;  // L(m) of the thread's last-pass rows: 0 / +CAP / -CAP
+    // frozen bits of the thread's rows, P bits per pass layout
+    using FzT = typename std::conditional<(Q * P > 32), unsigned long long, uint32_t>::type;
+    FzT fzp;
+    int frontier, nev, it, ph;
+    FzT snap;      // sign bits of R(S+1) after each stage of the current pass
+    uint32_t onm;  // PE activations of the current pass, bit i * P/2 + k
+    unsigned act;  // this thread's PE activations (< 2^32 per frame)
 
     template <int q>
     __device__ __forceinline__ int row(int j) const {
@@ -98,29 +171,95 @@ struct Dec {
         return (tid & ((1 << b) - 1)) | (j << b) | ((tid >> b) << (b + K));
     }
 
-    // stage S: PEs (j, j + dj) of this thread's registers; returns false when
-    // the csfg frontier covered n (the reference leaves the stage loop)
+    template <int q>
+    __device__ __forceinline__ void init_fz(const uint8_t* frozen_rows) {
+        if constexpr (q == 0) fzp = 0;
+#pragma unroll
+        for (int j = 0; j < P; ++j) fzp |= (FzT)(frozen_rows[row<q>(j)] != 0) << (q * P + j);
+        if constexpr (q + 1 < Q) init_fz<q + 1>(frozen_rows);
+    }
+    template <int q>
+    __device__ __forceinline__ uint32_t fz() const {
+        return (uint32_t)(fzp >> (q * P)) & low_mask(P);
+    }
+
+    // padded shared-memory index of row<q>(j): pad(row) = pad(row<q>(0)) +
+    // pad(j << b) (the register bits never carry into the thread bits), so
+    // every access is one per-pass base register plus an immediate
+    template <int q>
+    __device__ __forceinline__ int pbase() const {
+        return PL::pad(row<q>(0));
+    }
+    template <int q>
+    static constexpr int poff(int j) {
+        return PL::pad(j << PL::base(q));
+    }
+
+    template <int s, int q>
+    __device__ __forceinline__ float ld(int j) const {
+        constexpr int w = C::where(s);
+        if constexpr (w == kReg) return Lr[PL::slot(s)][j];
+        else if constexpr (w == kSmem) return sm->Ls[PL::slot(s)][pbase<q>() + poff<q>(j)];
+        else if constexpr (w == kGlob) return Lg[(size_t)PL::slot(s) * N + row<q>(j)];
+        else return ((lm_nz >> j) & 1u) ? (((lm_neg >> j) & 1u) ? -kCap : kCap) : 0.f;
+    }
+    template <int s, int q>
+    __device__ __forceinline__ void st(int j, float v) {
+        constexpr int w = C::where(s);
+        if constexpr (w == kReg) Lr[PL::slot(s)][j] = v;
+        else if constexpr (w == kSmem) sm->Ls[PL::slot(s)][pbase<q>() + poff<q>(j)] = v;
+        else if constexpr (w == kGlob) Lg[(size_t)PL::slot(s) * N + row<q>(j)] = v;
+        else {
+            lm_nz |= 1u << j;
+            lm_neg = v < 0.f ? (lm_neg | (1u << j)) : (lm_neg & ~(1u << j));
+        }
+    }
+
+    // x_hat bits of the thread's rows, bit j = (R[j] < 0) (R is never -0)
+    __device__ __forceinline__ uint32_t sign_bits() const {
+        uint32_t w = 0u;
+#pragma unroll
+        for (int j = P - 1; j >= 0; --j) w = __funnelshift_l(__float_as_uint(R[j]), w, 1);
+        return w;
+    }
+
+    // stage S; false when the csfg frontier covered n (the reference leaves
+    // the stage loop, csfg_freeze.cpp:109). csfg checks are deferred to the
+    // end of the pass (pass_check): the pass's stages run as if no check of
+    // the pass commits, and the commits correct that afterwards.
     template <int S>
     __device__ __forceinline__ bool stage() {
         constexpr int q = PL::pass_of(S);
         constexpr int b = PL::base(q);
         constexpr int g = M - 1 - S;
         constexpr int dj = 1 << (g - b);
+        constexpr int i = S - q * K;  // stage index inside the pass
         if constexpr (csfg) {
-            if (sm->frontier >= N) return false;
+            if (frontier >= N) return false;
+            if constexpr (i == 0) {
+                snap = 0;
+                onm = 0u;
+            }
         }
-        const float* Lin = L + (size_t)S * N;             // L(S+1)
-        float* Lout = L + (size_t)(S > 0 ? S - 1 : 0) * N;  // L(S)
-        // loads first (all PEs of the stage), then the math
         float lt[P / 2], lb[P / 2];
-        bool on[P / 2];
+        // is_pe_active (csfg_freeze.cpp:95-97) as a mask over the thread's
+        // PEs; rows >= frontier are never frozen, and row<q>(0) is the
+        // thread's lowest row
+        uint32_t onb = low_mask(P / 2);
+        if (csfg && row<q>(0) < frontier) {
+            const uint8_t* fs = sm->fst + row<q>(0);
+#pragma unroll
+            for (int j = 0, k = 0; j < P; ++j) {
+                if (j & dj) continue;
+                if (row<q>(j) < frontier && (int)fs[j << b] < S) onb &= ~(1u << k);
+                ++k;
+            }
+        }
 #pragma unroll
         for (int j = 0, k = 0; j < P; ++j) {
             if (j & dj) continue;
-            const int rt = row<q>(j);
-            on[k] = !csfg || (int)sm->fst[rt] >= S;  // is_pe_active (csfg_freeze.cpp:95-97)
-            lt[k] = on[k] ? Lin[rt] : 0.f;
-            lb[k] = on[k] ? Lin[rt + (1 << g)] : 0.f;
+            lt[k] = ld<S + 1, q>(j);
+            lb[k] = ld<S + 1, q>(j + dj);
             ++k;
         }
 #pragma unroll
@@ -128,27 +267,24 @@ struct Dec {
             if (j & dj) continue;
             const int rt = row<q>(j), rb = rt + (1 << g);
             bool xt = false, xb = false;
-            if (on[k]) {
+            if ((onb >> k) & 1u) {
                 const float r_t = R[j], r_b = R[j + dj];
                 const float cross = __fmul_rn(alpha, xsmin(lt[k], r_t));
                 const float sum_bot = __fadd_rn(lb[k], r_b);
                 const float l_top = __fmul_rn(alpha, xsmin(lt[k], sum_bot));
                 const float l_bot = __fadd_rn(lb[k], cross);
                 if constexpr (S > 0) {
-                    Lout[rt] = l_top;
-                    Lout[rb] = l_bot;
+                    st<S, q>(j, l_top);
+                    st<S, q>(j + dj, l_bot);
                 } else {  // L(0) only feeds the G-check's x_hat (bp_core.cpp:99)
                     xt = __fadd_rn(r_t, l_top) < 0.f;
                     xb = __fadd_rn(r_b, l_bot) < 0.f;
                 }
                 R[j] = __fmaf_rn(alpha, xsmin(r_t, sum_bot), 0.0f);
                 R[j + dj] = __fadd_rn(r_b, cross);
-                ++act;
             }
             if constexpr (S == 0 && KIND != 0) {
-                // pass 0 keeps row bits [0, 9) in the thread index: a warp's
-                // lanes hold 32 consecutive rows of every register
-                static_assert(PL::base(0) >= 5, "pass 0 layout");
+                // pass 0: a warp's lanes hold 32 consecutive rows of every register
                 const uint32_t wt = __ballot_sync(kFull, xt), wb = __ballot_sync(kFull, xb);
                 if (lane == 0) {
                     sm->xh[rt >> 5] = wt;
@@ -157,181 +293,260 @@ struct Dec {
             }
             ++k;
         }
-        if constexpr (csfg) return check<S>();
+        act += __popc(onb);
+        if constexpr (csfg) {
+            onm |= onb << (i * (P / 2));
+            snap |= (FzT)sign_bits() << (i * P);
+        }
+        constexpr bool pass_end = S == PL::last(q);
+        constexpr bool boundary = pass_end && q + 1 < Q;
+        // R(S+1) into the next pass's layout; it does not depend on the
+        // verdicts, so the check's barriers also order the exchange
+        if constexpr (boundary) {
+            if constexpr (!C::rx2) __syncthreads();  // readers of the previous boundary are done
+            float* rx = sm->Rx[C::rx2 ? (q & 1) : 0];
+#pragma unroll
+            for (int j = 0; j < P; ++j) rx[pbase<q>() + poff<q>(j)] = R[j];
+        }
+        if constexpr (csfg && pass_end) pass_check<q>();
+        if constexpr (boundary) {
+            if constexpr (!csfg) __syncthreads();
+            const float* rx = sm->Rx[C::rx2 ? (q & 1) : 0];
+#pragma unroll
+            for (int j = 0; j < P; ++j) R[j] = rx[pbase<q + 1>() + poff<q + 1>(j)];
+        }
         return true;
+    }
+
+    // lane bits [0, NL) of the transform by shuffles: the lower lane absorbs
+    template <int NL, typename W>
+    __device__ __forceinline__ W lane_transform(W w) const {
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+            const W v = __shfl_xor_sync(kFull, w, 1 << k);
+            if (!((lane >> k) & 1)) w ^= v;
+        }
+        return w;
+    }
+
+    // warp-index bits [0, NWB): XOR over the supersets, through shared memory
+    template <int NWB, typename W>
+    __device__ __forceinline__ W warp_transform(W w) {
+        sm->buf[tid] = w;
+        __syncthreads();
+        const int wl = warp & ((1 << NWB) - 1), wh = warp - wl;
+        W acc = 0;
+        for (int s = wl; s < (1 << NWB); s = (s + 1) | wl) acc ^= (W)sm->buf[(wh | s) * 32 + lane];
+        return acc;
+    }
+
+    // P-bit mask of the thread's rows (layout q) inside block `index` of size 2^g:
+    // row >> g = (thread-high bits << (b + K - g)) | (j >> (g - b))
+    template <int q, int g>
+    __device__ __forceinline__ uint32_t block_mask(int index) const {
+        constexpr int b = PL::base(q);
+        constexpr int hb = b + K - g;
+        const int jsel = index & ((1 << hb) - 1);
+        return (index >> hb) == (tid >> b) ? low_mask(1 << (g - b)) << (jsel << (g - b)) : 0u;
+    }
+
+    // in-thread transform levels of stage index i of pass q, into the packed word
+    template <int q, int i>
+    __device__ __forceinline__ FzT pass_bits() const {
+        constexpr int S = q * K + i;
+        if constexpr (S > PL::last(q)) {
+            return 0;
+        } else {
+            const uint32_t w = bits_transform<M - 1 - S - PL::base(q)>((uint32_t)(snap >> (i * P)) & low_mask(P));
+            return ((FzT)w << (i * P)) | pass_bits<q, i + 1>();
+        }
+    }
+
+    // violation bits of stage index i for every frontier the pass's earlier
+    // commits can produce: bit (2^i - 1 + v), v = the set of earlier stages
+    // that committed; f[] holds those frontiers (f[2^i - 1 + v])
+    template <int q, int i>
+    __device__ __forceinline__ uint32_t pass_viol(FzT W, int* f) const {
+        constexpr int S = q * K + i;
+        if constexpr (S > PL::last(q)) {
+            return 0u;
+        } else {
+            constexpr int g = M - 1 - S;
+            const uint32_t u = (uint32_t)(W >> (i * P)) & fz<q>();
+            uint32_t bad = 0u;
+#pragma unroll
+            for (int v = 0; v < (1 << i); ++v) {
+                const int fr = f[(1 << i) - 1 + v];
+                if (fr < N && (u & block_mask<q, g>(fr >> g)) != 0u) bad |= 1u << ((1 << i) - 1 + v);
+                // frontiers of stage i + 1: unchanged, or the end of this block
+                if constexpr (S < PL::last(q)) {
+                    f[(2 << i) - 1 + v] = fr;
+                    f[(2 << i) - 1 + v + (1 << i)] = ((fr >> g) + 1) << g;
+                }
+            }
+            return bad | pass_viol<q, i + 1>(W, f);
+        }
     }
 
     // candidate_block / check_csfg / apply_freeze (csfg_freeze.cpp:8-39,
-    // 82-93, 116-118) after stage S
-    template <int S>
-    __device__ __forceinline__ bool check() {
-        constexpr int q = PL::pass_of(S);
-#pragma unroll
-        for (int j = 0; j < P; ++j) sm->sgn[row<q>(j)] = __float_as_int(R[j]) < 0;
+    // 82-93, 116-118) for every stage of pass q, in the reference's order.
+    // The candidate transform of a stage is the same for every block of its
+    // size, so one transform per stage serves every frontier; lane and warp
+    // bits are shared by all of the pass's stages (their blocks span them).
+    template <int q>
+    __device__ __forceinline__ void pass_check() {
+        constexpr int b = PL::base(q);
+        constexpr int nst = PL::last(q) - q * K + 1;
+        FzT W = pass_bits<q, 0>();
+        W = lane_transform<(b < 5 ? b : 5)>(W);
+        if constexpr (b > 5) W = warp_transform<b - 5>(W);
+        int f[(1 << nst) - 1 + (1 << nst)];
+        f[0] = frontier;
+        uint32_t bad = pass_viol<q, 0>(W, f);
+        bad = __reduce_or_sync(kFull, bad);
+        if (lane == 0 && bad) atomicOr(&sm->vw[ph], bad);
         __syncthreads();
-        constexpr int g = M - 1 - S;
-        constexpr int sz = 1 << g;
-        constexpr int nw = (sz + 31) >> 5;
-        const int frontier = sm->frontier;
-        const int index = frontier >> g;
-        const int start = index << g;
-        if constexpr (sz > 32) {  // block bits by the CTA, one word per warp step
-            for (int i = tid; i < nw * 32; i += PL::T) {
-                const uint32_t w = __ballot_sync(kFull, sm->sgn[start + i] != 0);
-                if (lane == 0) sm->wb0[i >> 5] = w;
-            }
-            __syncthreads();
-        }
-        if (tid < 32) {
-            if constexpr (sz <= 32) {
-                const uint32_t w = __ballot_sync(kFull, lane < sz && sm->sgn[start + lane] != 0);
-                if (lane == 0) sm->wb0[0] = w;
-                __syncwarp();
-            }
-            warp_transform(sm->wb0, sz, lane);
-            bool viol = false;
-            if constexpr (sz >= 32) {
-                for (int w = lane; w < nw; w += 32) viol |= (sm->wb0[w] & sm->frz[(start >> 5) + w]) != 0u;
-            } else {
-                if (lane == 0) viol = (sm->wb0[0] & (sm->frz[start >> 5] >> (start & 31)) & low_mask(sz)) != 0u;
-            }
-            const bool acc = !__any_sync(kFull, viol);
-            if (lane == 0) sm->accept = acc ? 1 : 0;
-        }
-        __syncthreads();
-        if (!sm->accept) return true;
-        // apply_freeze: L(S+1) = +-CAP over the block, freeze_stage, decided_u, event
-        float* Lsat = L + (size_t)S * N;
-        for (int i = tid; i < sz; i += PL::T) {
-            const int r = start + i;
-            Lsat[r] = sm->sgn[r] ? -kCap : kCap;
-            if ((int)sm->fst[r] > S) sm->fst[r] = (uint8_t)S;
-        }
-        if constexpr (sz >= 32) {
-            for (int w = tid; w < nw; w += PL::T) sm->dec_u[(start >> 5) + w] = sm->wb0[w];
-        } else if (tid == 0) {
-            const int off = start & 31;
-            const uint32_t msk = low_mask(sz) << off;
-            sm->dec_u[start >> 5] = (sm->dec_u[start >> 5] & ~msk) | ((sm->wb0[0] << off) & msk);
-        }
-        __syncthreads();  // every thread read frontier/accept above
-        if (tid == 0) {
-            if (a->events && sm->nev < a->ev_cap) {
-                int* e = a->events + ((long long)sm->frame * a->ev_cap + sm->nev) * 5;
-                e[0] = it;
-                e[1] = S;
-                e[2] = index;
-                e[3] = start;
-                e[4] = sz;
-            }
-            sm->nev += 1;
-            sm->frontier = start + sz;
-        }
-        __syncthreads();
-        return true;
+        bad = sm->vw[ph];
+        if (tid == 0) sm->vw[ph == 0 ? 2 : ph - 1] = 0u;  // used two checks from now
+        ph = ph == 2 ? 0 : ph + 1;
+        if (bad == (1u << ((1 << nst) - 1)) - 1u) return;  // every candidate rejected
+        bool any = false;
+        commit_walk<q, 0>(W, bad, 0, any);
+        // freeze stages are read in another layout by the next pass
+        if (any) __syncthreads();
     }
 
-    int it = 0;
+    template <int q, int i>
+    __device__ __forceinline__ void commit_walk(FzT W, uint32_t bad, int v, bool& any) {
+        constexpr int S = q * K + i;
+        if constexpr (S <= PL::last(q)) {
+            if (frontier >= N) return;
+            if (!((bad >> ((1 << i) - 1 + v)) & 1u)) {
+                commit<q, i>(W);
+                v |= 1 << i;
+                any = true;
+            }
+            commit_walk<q, i + 1>(W, bad, v, any);
+        }
+    }
 
-    // pass boundaries move R through shared memory into the next layout
+    // apply_freeze of stage index i's candidate by the owners of its rows, and
+    // the PE activations of the pass's later stages that the commit made
+    // inactive (or, when the frontier reached n, that the reference never ran)
+    template <int q, int i>
+    __device__ __forceinline__ void commit(FzT W) {
+        constexpr int b = PL::base(q);
+        constexpr int S = q * K + i;
+        constexpr int g = M - 1 - S;
+        constexpr int sz = 1 << g;
+        const int index = frontier >> g;
+        const int start = index << g;
+        const uint32_t bm = block_mask<q, g>(index);
+        const uint32_t u = (uint32_t)(W >> (i * P));
+        const uint32_t x = (uint32_t)(snap >> (i * P));
+        if (bm) {
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                if (!((bm >> j) & 1u)) continue;
+                const int r = row<q>(j);
+                st<S + 1, q>(j, ((x >> j) & 1u) ? -kCap : kCap);
+                if ((int)sm->fst[r] > S) sm->fst[r] = (uint8_t)S;
+                const uint32_t bit = 1u << (r & 31);
+                if ((u >> j) & 1u) atomicOr(&sm->dec[r >> 5], bit);
+                else atomicAnd(&sm->dec[r >> 5], ~bit);
+            }
+        }
+        if (tid == 0 && a->events && nev < a->ev_cap) {
+            int* e = a->events + ((long long)sm->frame * a->ev_cap + nev) * 5;
+            e[0] = it;
+            e[1] = S;
+            e[2] = index;
+            e[3] = start;
+            e[4] = sz;
+        }
+        nev += 1;
+        frontier = start + sz;
+        uncount<q, i + 1>(bm, frontier >= N);
+    }
+
+    template <int q, int i>
+    __device__ __forceinline__ void uncount(uint32_t bm, bool all) {
+        constexpr int S = q * K + i;
+        if constexpr (S <= PL::last(q)) {
+            constexpr int dj = 1 << (M - 1 - S - PL::base(q));
+            uint32_t tm = 0u;  // top rows of stage S inside the block, as PE indices
+#pragma unroll
+            for (int j = 0, k = 0; j < P; ++j) {
+                if (j & dj) continue;
+                tm |= ((bm >> j) & 1u) << k;
+                ++k;
+            }
+            const uint32_t drop = (all ? low_mask(P / 2) : tm) << (i * (P / 2)) & onm;
+            act -= __popc(drop);
+            onm &= ~drop;
+            uncount<q, i + 1>(bm, all);
+        }
+    }
+
     template <int S>
     __device__ __forceinline__ bool sweep_from() {
-        constexpr int q = PL::pass_of(S);
-        if constexpr (S == PL::first(q) && q > 0) {
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < P; ++j) R[j] = sm->Rx[PL::pad(row<q>(j))];
-        }
         if (!stage<S>()) return false;
-        if constexpr (S == PL::last(q) && q + 1 < Q) {
-            __syncthreads();  // the previous boundary's readers are done
-#pragma unroll
-            for (int j = 0; j < P; ++j) sm->Rx[PL::pad(row<q>(j))] = R[j];
-        }
         if constexpr (S + 1 < M) return sweep_from<S + 1>();
         return true;
     }
 
-    // u_hat of the last sweep (frozen rows 0, rows < pin from decided_u) into
-    // wb0; R is in the last pass's layout (rows P*tid + j)
-    __device__ __forceinline__ void u_words(int pin) {
-        for (int w = tid; w < NW; w += PL::T) sm->wb0[w] = 0u;
-        __syncthreads();
-        if constexpr (P >= 32) {
-#pragma unroll
-            for (int c = 0; c < P / 32; ++c) {
-                uint32_t w = 0u;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) w |= (uint32_t)(__float_as_int(R[32 * c + i]) < 0) << i;
-                const int wi = (P * tid) / 32 + c;
-                w &= ~sm->frz[wi];
-                const int r0 = 32 * wi;
-                if (pin > r0) {
-                    const uint32_t pm = pin - r0 >= 32 ? kFull : low_mask(pin - r0);
-                    w = (w & ~pm) | (sm->dec_u[wi] & pm);
-                }
-                sm->wb0[wi] = w;
-            }
-        } else {
-            uint32_t w = 0u;
-#pragma unroll
-            for (int i = 0; i < P; ++i) w |= (uint32_t)(__float_as_int(R[i]) < 0) << i;
-            const int r0 = P * tid, wi = r0 >> 5, sh = r0 & 31;
-            const uint32_t m = low_mask(P);
-            w &= ~(sm->frz[wi] >> sh) & m;
-            if (pin > r0) {
-                const uint32_t pm = pin - r0 >= P ? m : low_mask(pin - r0);
-                w = (w & ~pm) | ((sm->dec_u[wi] >> sh) & pm);
-            }
-            atomicOr(&sm->wb0[wi], w << sh);
+    // hard_output with frozen rows 0 and rows < pin from decided_u, as the
+    // thread's P-bit group (rows P*tid + j; R in the last pass's layout)
+    __device__ __forceinline__ uint32_t u_group(int pin) const {
+        uint32_t u = sign_bits() & ~fz<Q - 1>();
+        const int r0 = P * tid;
+        if (pin > r0) {
+            const uint32_t pm = pin - r0 >= P ? low_mask(P) : low_mask(pin - r0);
+            const uint32_t d = (sm->dec[r0 >> 5] >> (r0 & 31)) & low_mask(P);
+            u = (u & ~pm) | (d & pm);
         }
-        __syncthreads();
+        return u;
     }
 
     // gmatrix_converged (bp_core.cpp:95-102) with the pinned prefix
-    // (csfg_freeze.cpp:120-135)
+    // (csfg_freeze.cpp:120-135): the transform over all n row bits (register
+    // bits [0, K), lane bits [K, K+5), warp bits above), compared to x_hat
     __device__ __forceinline__ bool gcheck(int pin) {
-        u_words(pin);
-        if (tid < 32) {
-            warp_transform(sm->wb0, N, lane);
-            bool diff = false;
-            for (int w = lane; w < NW; w += 32) diff |= sm->wb0[w] != sm->xh[w];
-            const bool c = !__any_sync(kFull, diff);
-            if (lane == 0) sm->conv = c ? 1 : 0;
-        }
-        __syncthreads();
-        return sm->conv != 0;
+        uint32_t u = bits_transform<K>(u_group(pin));
+        u = lane_transform<5>(u);
+        u = warp_transform<PL::LOGT - 5>(u);
+        const int r0 = P * tid;
+        const uint32_t x = (sm->xh[r0 >> 5] >> (r0 & 31)) & low_mask(P);
+        return !__syncthreads_or(u != x);
     }
 
-    __device__ void run(const DecodeArgs& args, CtaSmem<M>* s) {
+    __device__ void run(const DecodeArgs& args, Smem<M>* s) {
         a = &args;
         sm = s;
         tid = threadIdx.x;
         lane = tid & 31;
+        warp = tid >> 5;
         alpha = args.alpha;
-        L = args.scratch + (long long)blockIdx.x * args.scratch_stride;
-        for (int w = tid; w < NW; w += PL::T) sm->frz[w] = args.frozen_bits[w];
+        Lg = args.scratch + (long long)blockIdx.x * args.scratch_stride;
+        init_fz<0>(args.frozen_rows);
         for (;;) {
             __syncthreads();
             if (tid == 0) {
                 const unsigned long long idx = atomicAdd(args.queue, 1ull);
                 sm->frame = (long long)idx < args.frames ? (long long)idx : -1;
-                sm->frontier = 0;
-                sm->nev = 0;
-                sm->act = 0ull;
-                sm->bit_err = 0;
             }
             __syncthreads();
             const long long f = sm->frame;
             if (f < 0) break;
-            // channel LLRs (R(0), -0 -> +0) in pass 0's layout; frames beyond the
-            // clamp-free bound go to the generic kernel
-            const float* llr = args.llr + f * (long long)N;
+            // channel LLRs (R(0), -0 -> +0) in pass 0's layout; frames beyond
+            // the clamp-free bound go to the generic kernel
+            llr = args.llr + f * (long long)N;
             bool bad = false;
 #pragma unroll
             for (int j = 0; j < P; ++j) {
                 const float v = llr[row<0>(j)];
                 bad |= !(fabsf(v) <= kClampFreeBound);
+                if constexpr (C::r0reg) R0[j] = __fadd_rn(v, 0.0f);
             }
             if (__syncthreads_or(bad)) {
                 if (tid == 0) {
@@ -341,14 +556,20 @@ struct Dec {
                 continue;
             }
             // init_state (bp_core.cpp:43-56)
-            for (int r = tid; r < N; r += PL::T) {
-                for (int l = 1; l < M; ++l) L[(size_t)(l - 1) * N + r] = 0.f;
-                L[(size_t)(M - 1) * N + r] = args.frozen_rows[r] ? kCap : 0.f;
-                sm->fst[r] = kNotFrozen;
-            }
-            for (int w = tid; w < NW; w += PL::T) sm->dec_u[w] = 0u;
 #pragma unroll
-            for (int j = 0; j < P; ++j) R[j] = 0.f;
+            for (int l = 0; l < PL::NREG; ++l)
+#pragma unroll
+                for (int j = 0; j < P; ++j) Lr[l][j] = 0.f;
+            lm_nz = fz<Q - 1>();
+            lm_neg = 0u;
+            for (int i = tid; i < PL::NSM * PL::NX; i += kT) (&sm->Ls[0][0])[i] = 0.f;
+            for (int i = tid; i < PL::NGL * N; i += kT) Lg[i] = 0.f;
+            for (int r = tid; r < N; r += kT) sm->fst[r] = kNotFrozen;
+            for (int w = tid; w < NW; w += kT) sm->dec[w] = 0u;
+            frontier = 0;
+            nev = 0;
+            ph = 0;
+            if (tid < 3) sm->vw[tid] = 0u;
             act = 0;
             __syncthreads();
             int iters = (KIND == 0) ? args.max_iter : 0;
@@ -356,66 +577,78 @@ struct Dec {
             bool converged = false;
             for (int t = 1; t <= args.max_iter; ++t) {
                 if constexpr (csfg) {
-                    if (sm->frontier >= N || converged) break;
+                    if (frontier >= N || converged) break;
                     iters = t;
                 }
                 it = t;
+                // keep the per-stage row/address arithmetic inside the loop
+                // (hoisted for every stage it would not fit in the registers)
+                asm volatile("" : "+r"(tid));
 #pragma unroll
-                for (int j = 0; j < P; ++j) R[j] = __fadd_rn(llr[row<0>(j)], 0.0f);
+                for (int j = 0; j < P; ++j) {
+                    if constexpr (C::r0reg) R[j] = R0[j];
+                    else R[j] = __fadd_rn(llr[row<0>(j)], 0.0f);
+                }
                 sweep_from<0>();
-                __syncthreads();
-                if constexpr (KIND == 1) {
+                if constexpr (KIND == 0) {
+                    __syncthreads();  // Rx buffers are reused by the next sweep
+                } else if constexpr (KIND == 1) {
                     if (gcheck(0)) {
                         iters = t;
                         stop = 1;
                         break;
                     }
-                } else if constexpr (csfg) {
-                    const int pin = sm->frontier;
-                    if (pin < N) converged = gcheck(pin);
+                } else {
+                    if (frontier < N) converged = gcheck(frontier);
                 }
             }
             if constexpr (KIND == 1) {
                 if (stop == 0) iters = args.max_iter;
             }
-            const int frontier = sm->frontier;
             if constexpr (csfg) stop = (frontier >= N) ? 2 : (converged ? 1 : 0);
-            const int pin = csfg ? (frontier >= N ? N : frontier) : 0;
             // DecodeOutcome (bp_core.cpp:106-115, csfg_freeze.cpp:137-151)
-            if (csfg && frontier >= N) {
-                __syncthreads();
-                for (int w = tid; w < NW; w += PL::T) sm->wb0[w] = sm->dec_u[w];
-                __syncthreads();
-            } else {
-                u_words(pin);
-            }
+            __syncthreads();  // decided_u of the last commits
+            uint32_t u;
+            const int r0 = P * tid;
+            if (csfg && frontier >= N) u = (sm->dec[r0 >> 5] >> (r0 & 31)) & low_mask(P);
+            else u = u_group(csfg ? frontier : 0);
+            // the P-bit groups of 32/P consecutive threads form one word
+            uint32_t word = u << (r0 & 31);
+#pragma unroll
+            for (int o = 1; o < 32 / P; o <<= 1) word |= __shfl_xor_sync(kFull, word, o);
             int berr = 0;
-            for (int w = tid; w < NW; w += PL::T) {
-                const uint32_t uw = sm->wb0[w];
-                if (args.u_bits) args.u_bits[f * NW + w] = uw;
-                if (args.truth_u) berr += __popc((uw ^ args.truth_u[f * NW + w]) & ~sm->frz[w]);
+            if ((r0 & 31) == 0) {
+                const int wi = r0 >> 5;
+                if (args.u_bits) args.u_bits[f * NW + wi] = word;
+                if (args.truth_u) berr = __popc((word ^ args.truth_u[f * NW + wi]) & ~args.frozen_bits[wi]);
             }
             berr = __reduce_add_sync(kFull, berr);
-            const long long wact = __reduce_add_sync(kFull, (unsigned)act);  // < 2^32 per thread
+            const unsigned wact = __reduce_add_sync(kFull, act);
+            // per-CTA sums through shared memory (buf: no transform is pending)
             if (lane == 0) {
-                if (berr) atomicAdd(&sm->bit_err, berr);
-                atomicAdd(&sm->act, (unsigned long long)wact);
+                sm->buf[2 * warp] = (uint32_t)berr;
+                sm->buf[2 * warp + 1] = wact;
             }
             __syncthreads();
             if (tid == 0) {
-                const long long pe = (long long)sm->act;
+                long long pe = 0;
+                int be = 0;
+                for (int w = 0; w < PL::NWARP; ++w) {
+                    be += (int)sm->buf[2 * w];
+                    pe += sm->buf[2 * w + 1];
+                }
                 if (args.iters) args.iters[f] = iters;
                 if (args.pe) args.pe[f] = pe;
                 if (args.stop) args.stop[f] = (uint8_t)stop;
-                if (args.nev) args.nev[f] = sm->nev;
+                if (args.nev) args.nev[f] = nev;
                 if (args.counters) {
                     atomicAdd(&args.counters[kCntFrames], 1ull);
-                    atomicAdd(&args.counters[kCntBitErr], (unsigned long long)sm->bit_err);
-                    atomicAdd(&args.counters[kCntFrameErr], sm->bit_err > 0 ? 1ull : 0ull);
+                    atomicAdd(&args.counters[kCntBitErr], (unsigned long long)be);
+                    atomicAdd(&args.counters[kCntFrameErr], be > 0 ? 1ull : 0ull);
                     atomicAdd(&args.counters[kCntIters], (unsigned long long)iters);
                     atomicAdd(&args.counters[kCntItersSq], (unsigned long long)iters * iters);
                     atomicAdd(&args.counters[kCntPe], (unsigned long long)pe);
-                    atomicAdd(&args.counters[kCntEvents], (unsigned long long)sm->nev);
+                    atomicAdd(&args.counters[kCntEvents], (unsigned long long)nev);
                     atomicAdd(&args.counters[kCntStop0 + stop], 1ull);
                 }
             }
@@ -423,25 +656,20 @@ struct Dec {
     }
 };
 
-// 64 registers: two 512-thread frames per SM up to n = 4096, one 1024-thread
-// frame beyond
-template <int M>
-constexpr int kMinCtas = M <= 12 ? 2 : 1;
-
 template <int M, int KIND>
-__global__ void __launch_bounds__(CPlan<M>::T, kMinCtas<M>) bp_cta_kernel(DecodeArgs a) {
+__global__ void __launch_bounds__(Plan<M>::T, Cfg<M>::MINB) bp_cta_kernel(const __grid_constant__ DecodeArgs a) {
     extern __shared__ __align__(16) unsigned char csm[];
     Dec<M, KIND> dec;
-    dec.run(a, reinterpret_cast<CtaSmem<M>*>(csm));
+    dec.run(a, reinterpret_cast<Smem<M>*>(csm));
 }
 
 template <int M, int KIND>
 static cudaError_t launch_t(const DecodeArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = sizeof(CtaSmem<M>);
+    const size_t smem = sizeof(Smem<M>);
     cudaError_t e = cudaFuncSetAttribute(bp_cta_kernel<M, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    bp_cta_kernel<M, KIND><<<grid, CPlan<M>::T, smem, st>>>(a);
+    bp_cta_kernel<M, KIND><<<grid, Plan<M>::T, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -457,9 +685,9 @@ static cudaError_t launch_m(const DecodeArgs& a, int grid, cudaStream_t st) {
 template <int M, int KIND>
 static int occ_t() {
     int nb = 0;
-    const size_t smem = sizeof(CtaSmem<M>);
+    const size_t smem = sizeof(Smem<M>);
     cudaFuncSetAttribute(bp_cta_kernel<M, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bp_cta_kernel<M, KIND>, CPlan<M>::T, smem) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bp_cta_kernel<M, KIND>, Plan<M>::T, smem) != cudaSuccess)
         return 0;
     return nb;
 }
@@ -473,7 +701,16 @@ static int occ_m(int kind) {
 
 int cta_kernel_supported(int m) { return m >= 11 && m <= 14; }
 
-long long cta_scratch_floats(int m) { return (long long)m << m; }  // L(1..m)
+// L2-resident L levels per CTA (at least one level, so the pointer is valid)
+long long cta_scratch_floats(int m) {
+    switch (m) {
+        case 11: return (long long)std::max(1, cta::Plan<11>::NGL) << 11;
+        case 12: return (long long)std::max(1, cta::Plan<12>::NGL) << 12;
+        case 13: return (long long)std::max(1, cta::Plan<13>::NGL) << 13;
+        case 14: return (long long)std::max(1, cta::Plan<14>::NGL) << 14;
+    }
+    return 0;
+}
 
 cudaError_t launch_cta(const DecodeArgs& a, int grid, cudaStream_t st) {
     switch (a.m) {

@@ -1,5 +1,5 @@
 """Aggregate ncu warp-stall samples of one kernel by source line and enclosing function.
-   python tools/ncu_lines.py report.ncu-rep [source.cu] [--top 30]
+   python tools/ncu_lines.py report.ncu-rep [source.cu] [--top 30] [--by-inst]
 The report must be captured with -lineinfo builds and --import-source on. Samples are
 attributed to the innermost inlined line; functions are found by scanning the source for
 definitions, so helpers shared by several callers show up under their own name."""
@@ -9,6 +9,7 @@ from collections import defaultdict
 rep = sys.argv[1]
 src = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("--") else None
 top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 30
+by_inst = "--by-inst" in sys.argv  # rank lines by executed warp instructions
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True, check=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
@@ -60,7 +61,11 @@ for f, (n, ins, st) in sorted(byfn.items(), key=lambda kv: -kv[1][0]):
     print(f"{f:24s} {n:8d} {100*n/max(tot,1):6.1f} {ins:12d}  " +
           " ".join(f"{c[6:]}={100*v/max(n,1):.0f}%" for c, v in tops))
 print()
-for (p, ln), (s, n, ins, st) in sorted(lines.items(), key=lambda kv: -kv[1][1])[:top]:
+tot_ins = sum(v[2] for v in lines.values())
+for (p, ln), (s, n, ins, st) in sorted(lines.items(), key=lambda kv: -kv[1][2 if by_inst else 1])[:top]:
     tops = sorted(st.items(), key=lambda kv: -kv[1])[:3]
+    if by_inst:
+        print(f"{ln:5d} {ins:11d} {100*ins/max(tot_ins,1):5.1f}% {s.strip()[:90]}")
+        continue
     print(f"{ln:5d} {n:7d} {100*n/max(tot,1):5.1f}% {s.strip()[:70]:70s} " +
           " ".join(f"{c[6:]}={v}" for c, v in tops))
