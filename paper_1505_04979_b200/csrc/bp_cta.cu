@@ -267,22 +267,27 @@ struct Dec {
             if (j & dj) continue;
             const int rt = row<q>(j), rb = rt + (1 << g);
             bool xt = false, xb = false;
-            if ((onb >> k) & 1u) {
-                const float r_t = R[j], r_b = R[j + dj];
-                const float cross = __fmul_rn(alpha, xsmin(lt[k], r_t));
-                const float sum_bot = __fadd_rn(lb[k], r_b);
-                const float l_top = __fmul_rn(alpha, xsmin(lt[k], sum_bot));
-                const float l_bot = __fadd_rn(lb[k], cross);
-                if constexpr (S > 0) {
+            // every PE is computed; an inactive one keeps R and L unchanged
+            // (selects and predicated stores instead of a branch per PE)
+            const bool on = (onb >> k) & 1u;
+            const float r_t = R[j], r_b = R[j + dj];
+            const float cross = __fmul_rn(alpha, xsmin(lt[k], r_t));
+            const float sum_bot = __fadd_rn(lb[k], r_b);
+            const float l_top = __fmul_rn(alpha, xsmin(lt[k], sum_bot));
+            const float l_bot = __fadd_rn(lb[k], cross);
+            if constexpr (S > 0) {
+                if (on) {
                     st<S, q>(j, l_top);
                     st<S, q>(j + dj, l_bot);
-                } else {  // L(0) only feeds the G-check's x_hat (bp_core.cpp:99)
-                    xt = __fadd_rn(r_t, l_top) < 0.f;
-                    xb = __fadd_rn(r_b, l_bot) < 0.f;
                 }
-                R[j] = __fmaf_rn(alpha, xsmin(r_t, sum_bot), 0.0f);
-                R[j + dj] = __fadd_rn(r_b, cross);
+            } else {  // L(0) only feeds the G-check's x_hat (bp_core.cpp:99); stage 0 is always active
+                xt = __fadd_rn(r_t, l_top) < 0.f;
+                xb = __fadd_rn(r_b, l_bot) < 0.f;
             }
+            const float n_t = __fmaf_rn(alpha, xsmin(r_t, sum_bot), 0.0f);
+            const float n_b = __fadd_rn(r_b, cross);
+            R[j] = on ? n_t : r_t;
+            R[j + dj] = on ? n_b : r_b;
             if constexpr (S == 0 && KIND != 0) {
                 // pass 0: a warp's lanes hold 32 consecutive rows of every register
                 const uint32_t wt = __ballot_sync(kFull, xt), wb = __ballot_sync(kFull, xb);
@@ -336,7 +341,10 @@ struct Dec {
         __syncthreads();
         const int wl = warp & ((1 << NWB) - 1), wh = warp - wl;
         W acc = 0;
-        for (int s = wl; s < (1 << NWB); s = (s + 1) | wl) acc ^= (W)sm->buf[(wh | s) * 32 + lane];
+        const auto* col = sm->buf + wh * 32 + lane;
+#pragma unroll
+        for (int s = 0; s < (1 << NWB); ++s)
+            if ((s & wl) == wl) acc ^= (W)col[s * 32];
         return acc;
     }
 
@@ -364,20 +372,30 @@ struct Dec {
 
     // violation bits of stage index i for every frontier the pass's earlier
     // commits can produce: bit (2^i - 1 + v), v = the set of earlier stages
-    // that committed; f[] holds those frontiers (f[2^i - 1 + v])
+    // that committed; f[] holds those frontiers (f[2^i - 1 + v]). A block of
+    // 2^g rows covers nb = 2^(g-b) of the thread's registers: fold the
+    // violations of each group, then a frontier fr selects group
+    // (fr >> b) & (P - nb) when its thread bits (fr >> (b+K)) are the
+    // thread's own (never true for fr >= n).
     template <int q, int i>
     __device__ __forceinline__ uint32_t pass_viol(FzT W, int* f) const {
         constexpr int S = q * K + i;
         if constexpr (S > PL::last(q)) {
             return 0u;
         } else {
+            constexpr int b = PL::base(q);
             constexpr int g = M - 1 - S;
-            const uint32_t u = (uint32_t)(W >> (i * P)) & fz<q>();
+            constexpr int nb = 1 << (g - b);
+            uint32_t u = (uint32_t)(W >> (i * P)) & fz<q>();
+#pragma unroll
+            for (int h = 1; h < nb; h <<= 1) u |= u >> h;
+            const int th = tid >> b;
             uint32_t bad = 0u;
 #pragma unroll
             for (int v = 0; v < (1 << i); ++v) {
                 const int fr = f[(1 << i) - 1 + v];
-                if (fr < N && (u & block_mask<q, g>(fr >> g)) != 0u) bad |= 1u << ((1 << i) - 1 + v);
+                const int t = fr >> b;
+                bad |= (((t >> K) == th ? u : 0u) >> (t & (P - nb)) & 1u) << ((1 << i) - 1 + v);
                 // frontiers of stage i + 1: unchanged, or the end of this block
                 if constexpr (S < PL::last(q)) {
                     f[(2 << i) - 1 + v] = fr;
