@@ -104,7 +104,7 @@ struct WarpSmem {
     using PL = Plan<M>;
     float X[PL::Q - 1][PL::NX];            // pass boundaries: R(e) then L(e), padded rows
     float4 Ls[PL::NLS][PL::P / 4][32];     // lane-private L slots (last pass, n=1024)
-    float4 LM[PL::P / 4][32];              // L(m), lane-private, last-pass layout
+    uint32_t lmz[32], lmn[32];             // L(m) in {0, +-CAP}: nonzero / negative bits per lane (last-pass layout)
     uint32_t pm[PL::NLR + PL::NLS][32];    // per lane: rows whose L(s) is a frozen boundary
     uint32_t ss[PL::NLR][32];              // ... and their signs (register arrays)
     uint32_t dec_u[PL::NW];                // decided_u bits (row order)
@@ -250,14 +250,9 @@ struct Dec {
     __device__ __forceinline__ void load_L(float (&Lt)[P]) {
         constexpr int q = PL::pass_of(T - 1);
         if constexpr (T == M) {
+            const uint32_t z = sm->lmz[lane], ng = sm->lmn[lane];
 #pragma unroll
-            for (int c = 0; c < P / 4; ++c) {
-                const float4 v = sm->LM[c][lane];
-                Lt[4 * c] = v.x;
-                Lt[4 * c + 1] = v.y;
-                Lt[4 * c + 2] = v.z;
-                Lt[4 * c + 3] = v.w;
-            }
+            for (int j = 0; j < P; ++j) Lt[j] = ((z >> j) & 1u) ? (((ng >> j) & 1u) ? -kCap : kCap) : 0.f;
         } else if constexpr (PL::is_boundary(T)) {
             x_load<q>(sm->X[PL::pass_of(T) - 1], Lt);
         } else if constexpr (PL::local_reg(T)) {
@@ -740,8 +735,13 @@ struct Dec {
             const uint32_t xbits = (xx >> j0) & wm, ubits = (uu >> j0) & wm;
             // 1. saturate / protect L(S+1) (csfg_freeze.cpp:84-86)
             const int T = S + 1;
-            if (T == M || ((SMEMM >> T) & 1u)) {
-                float4* base = (T == M) ? &sm->LM[0][0] : &sm->Ls[__popc(SMEMM & ((1u << T) - 1u))][0][0];
+            if (T == M) {  // stage m-1 commits are last-pass commits (apply_last); kept for completeness
+                if (in_block) {
+                    sm->lmz[lane] |= wm << j0;
+                    sm->lmn[lane] = (sm->lmn[lane] & ~(wm << j0)) | (xbits << j0);
+                }
+            } else if ((SMEMM >> T) & 1u) {
+                float4* base = &sm->Ls[__popc(SMEMM & ((1u << T) - 1u))][0][0];
                 if (in_block) {
                     if (W >= 4) {
 #pragma unroll 1
@@ -867,9 +867,11 @@ struct Dec {
         if (Sr >= 0) {
             const int T = Sr + 1;
             const int owner = r / P, j = r % P;  // last-pass layout: row = P*lane + j
-            if (T == M || ((SMEMM >> T) & 1u)) {
-                float* base = (T == M) ? reinterpret_cast<float*>(&sm->LM[0][0])
-                                       : reinterpret_cast<float*>(&sm->Ls[__popc(SMEMM & ((1u << T) - 1u))][0][0]);
+            if (T == M) {  // one row per iteration: a plain read-modify-write of the owner's bits
+                sm->lmz[owner] |= 1u << j;
+                sm->lmn[owner] = (sm->lmn[owner] & ~(1u << j)) | (xbit << j);
+            } else if ((SMEMM >> T) & 1u) {
+                float* base = reinterpret_cast<float*>(&sm->Ls[__popc(SMEMM & ((1u << T) - 1u))][0][0]);
                 base[((j >> 2) * 32 + owner) * 4 + (j & 3)] = xbit ? -kCap : kCap;
             }
             sm->fst[r] = (uint8_t)Sr;
@@ -1246,11 +1248,8 @@ struct Dec {
 #pragma unroll 1
             for (int i = lane; i < PL::NX; i += 32) sm->X[x][i] = 0.f;
         // L(m): +CAP at frozen rows (bp_core.cpp:53), last-pass layout
-        const uint32_t fl = FZ[Q - 1];
-#pragma unroll 1
-        for (int c = 0; c < P / 4; ++c)
-            sm->LM[c][lane] = make_float4(((fl >> (4 * c)) & 1u) ? kCap : 0.f, ((fl >> (4 * c + 1)) & 1u) ? kCap : 0.f,
-                                          ((fl >> (4 * c + 2)) & 1u) ? kCap : 0.f, ((fl >> (4 * c + 3)) & 1u) ? kCap : 0.f);
+        sm->lmz[lane] = FZ[Q - 1];
+        sm->lmn[lane] = 0u;
         if (lane < NW) sm->dec_u[lane] = 0u;
 #pragma unroll 1
         for (int x = 0; x < Q - 1; ++x)
