@@ -99,12 +99,15 @@ struct Plan {
     static constexpr int NL = M - SL;       // stages in the last pass
 };
 
-template <int M>
+// LMB: L(m) as bit masks (csfg: frees 3.8 KB for an 8th warp per SM at n =
+// 1024); float4 slots otherwise (measured faster for the other decoders)
+template <int M, bool LMB = false>
 struct WarpSmem {
     using PL = Plan<M>;
     float X[PL::Q - 1][PL::NX];            // pass boundaries: R(e) then L(e), padded rows
     float4 Ls[PL::NLS][PL::P / 4][32];     // lane-private L slots (last pass, n=1024)
-    uint32_t lmz[32], lmn[32];             // L(m) in {0, +-CAP}: nonzero / negative bits per lane (last-pass layout)
+    float4 LM[LMB ? 1 : PL::P / 4][32];    // L(m), lane-private, last-pass layout (float slots)
+    uint32_t lmz[32], lmn[32];             // L(m) in {0, +-CAP}: nonzero / negative bits per lane (LMB)
     uint32_t pm[PL::NLR + PL::NLS][32];    // per lane: rows whose L(s) is a frozen boundary
     uint32_t ss[PL::NLR][32];              // ... and their signs (register arrays)
     uint32_t dec_u[PL::NW];                // decided_u bits (row order)
@@ -186,7 +189,8 @@ struct Dec {
     using PL = Plan<M>;
     static constexpr int N = PL::N, P = PL::P, K = PL::K, Q = PL::Q, NW = PL::NW;
 
-    WarpSmem<M>* sm;
+    using Smem = WarpSmem<M, KIND == 2>;
+    Smem* sm;
     float4* r0g;  // this warp's channel LLRs in global scratch, lane-private pass-0 layout
     const DecodeArgs* a;
     int lane;
@@ -249,10 +253,19 @@ struct Dec {
     template <int T>
     __device__ __forceinline__ void load_L(float (&Lt)[P]) {
         constexpr int q = PL::pass_of(T - 1);
-        if constexpr (T == M) {
+        if constexpr (T == M && KIND == 2) {
             const uint32_t z = sm->lmz[lane], ng = sm->lmn[lane];
 #pragma unroll
             for (int j = 0; j < P; ++j) Lt[j] = ((z >> j) & 1u) ? (((ng >> j) & 1u) ? -kCap : kCap) : 0.f;
+        } else if constexpr (T == M) {
+#pragma unroll
+            for (int c = 0; c < P / 4; ++c) {
+                const float4 v = sm->LM[c][lane];
+                Lt[4 * c] = v.x;
+                Lt[4 * c + 1] = v.y;
+                Lt[4 * c + 2] = v.z;
+                Lt[4 * c + 3] = v.w;
+            }
         } else if constexpr (PL::is_boundary(T)) {
             x_load<q>(sm->X[PL::pass_of(T) - 1], Lt);
         } else if constexpr (PL::local_reg(T)) {
@@ -1064,7 +1077,7 @@ struct Dec {
         return !__any_sync(kFull, lane < NW && uw != xw);
     }
 
-    __device__ __forceinline__ void run(const DecodeArgs& args, WarpSmem<M>* s, int ln) {
+    __device__ __forceinline__ void run(const DecodeArgs& args, Smem* s, int ln) {
         a = &args;
         r0g = reinterpret_cast<float4*>(args.r0s) + (long long)blockIdx.x * (N / 4);
         sm = s;
@@ -1248,8 +1261,17 @@ struct Dec {
 #pragma unroll 1
             for (int i = lane; i < PL::NX; i += 32) sm->X[x][i] = 0.f;
         // L(m): +CAP at frozen rows (bp_core.cpp:53), last-pass layout
-        sm->lmz[lane] = FZ[Q - 1];
-        sm->lmn[lane] = 0u;
+        if constexpr (KIND == 2) {
+            sm->lmz[lane] = FZ[Q - 1];
+            sm->lmn[lane] = 0u;
+        } else {
+            const uint32_t fl = FZ[Q - 1];
+#pragma unroll 1
+            for (int c = 0; c < P / 4; ++c)
+                sm->LM[c][lane] = make_float4(((fl >> (4 * c)) & 1u) ? kCap : 0.f, ((fl >> (4 * c + 1)) & 1u) ? kCap : 0.f,
+                                              ((fl >> (4 * c + 2)) & 1u) ? kCap : 0.f,
+                                              ((fl >> (4 * c + 3)) & 1u) ? kCap : 0.f);
+        }
         if (lane < NW) sm->dec_u[lane] = 0u;
 #pragma unroll 1
         for (int x = 0; x < Q - 1; ++x)
@@ -1271,26 +1293,27 @@ template <int M, int KIND>
 __global__ void __launch_bounds__(32, kMinWarps<M>) bp_warp_kernel(DecodeArgs a) {
     extern __shared__ __align__(16) unsigned char wsm[];
     Dec<M, KIND> dec;
-    dec.run(a, reinterpret_cast<WarpSmem<M>*>(wsm), threadIdx.x & 31);
+    dec.run(a, reinterpret_cast<typename Dec<M, KIND>::Smem*>(wsm), threadIdx.x & 31);
 }
 
 }  // namespace wk
 
 int warp_kernel_supported(int m) { return m >= 7 && m <= 10; }
 
-size_t warp_smem_bytes(int m) {
+size_t warp_smem_bytes(int m, int kind) {
+    const bool b = kind == 2;
     switch (m) {
-        case 7: return sizeof(wk::WarpSmem<7>);
-        case 8: return sizeof(wk::WarpSmem<8>);
-        case 9: return sizeof(wk::WarpSmem<9>);
-        case 10: return sizeof(wk::WarpSmem<10>);
+        case 7: return b ? sizeof(wk::WarpSmem<7, true>) : sizeof(wk::WarpSmem<7>);
+        case 8: return b ? sizeof(wk::WarpSmem<8, true>) : sizeof(wk::WarpSmem<8>);
+        case 9: return b ? sizeof(wk::WarpSmem<9, true>) : sizeof(wk::WarpSmem<9>);
+        case 10: return b ? sizeof(wk::WarpSmem<10, true>) : sizeof(wk::WarpSmem<10>);
     }
     return 0;
 }
 
 template <int M, int KIND>
 static cudaError_t launch_w(const DecodeArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = sizeof(wk::WarpSmem<M>);
+    const size_t smem = sizeof(typename wk::Dec<M, KIND>::Smem);
     cudaError_t e = cudaFuncSetAttribute(wk::bp_warp_kernel<M, KIND>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1320,7 +1343,7 @@ cudaError_t launch_warp(const DecodeArgs& a, int grid, cudaStream_t st) {
 template <int M, int KIND>
 static int occ_w() {
     int nb = 0;
-    const size_t smem = sizeof(wk::WarpSmem<M>);
+    const size_t smem = sizeof(typename wk::Dec<M, KIND>::Smem);
     cudaFuncSetAttribute(wk::bp_warp_kernel<M, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wk::bp_warp_kernel<M, KIND>, 32, smem) != cudaSuccess)
         return 0;

@@ -24,7 +24,7 @@ bool generic_in_smem(int n, int m, bool f64);
 cudaError_t launch_warp(const DecodeArgs& a, int grid, cudaStream_t st);
 int warp_kernel_supported(int m);
 int warp_blocks_per_sm(int m, int kind);
-size_t warp_smem_bytes(int m);
+size_t warp_smem_bytes(int m, int kind);
 int cta_kernel_supported(int m);
 long long cta_scratch_floats(int m);
 cudaError_t launch_cta(const DecodeArgs& a, int grid, cudaStream_t st);
@@ -520,7 +520,7 @@ int pbp_ctx_synchronize(pbp_ctx* ctx) {
 int pbp_kernel_info(int32_t n, int decoder, int32_t* smem_bytes, int32_t* warps_per_sm) {
     if (!is_pow2(n)) return fail(PBP_EINVAL, "pbp_kernel_info: n must be a power of two");
     const int m = log2i(n);
-    if (smem_bytes) *smem_bytes = pbp::warp_kernel_supported(m) ? (int32_t)pbp::warp_smem_bytes(m) : 0;
+    if (smem_bytes) *smem_bytes = pbp::warp_kernel_supported(m) ? (int32_t)pbp::warp_smem_bytes(m, decoder) : 0;
     if (warps_per_sm) *warps_per_sm = pbp::warp_kernel_supported(m) ? pbp::warp_blocks_per_sm(m, decoder) : 0;
     return PBP_OK;
 }

@@ -54,6 +54,18 @@ def main():
             chunk = min(frames, max(1, (1 << 28) // n))
             llr = torch.empty((chunk, n), dtype=torch.float32, device=dev)
             u = torch.empty((chunk, nw), dtype=torch.int32, device=dev)
+            # untimed warm-up: the first decode of a code length sizes the context's buffers
+            wcnt = torch.zeros(10, dtype=torch.int64, device=dev)
+            P._check(P.lib.pbp_generate_device(ctx.handle, C.byref(cs), C.c_uint64(seed), 0, chunk, snrs[0], 0,
+                                               P._abi.f32p(llr.data_ptr()), None, P._abi.u32p(u.data_ptr()),
+                                               C.c_void_p(stream.cuda_stream)))
+            P._check(P.lib.pbp_decode_count_device(ctx.handle, C.byref(cs), kind, P._abi.f32p(llr.data_ptr()),
+                                                   P._abi.u32p(u.data_ptr()), chunk, ALPHA, max_iter,
+                                                   P._abi.i64p(wcnt.data_ptr()), C.c_void_p(stream.cuda_stream)))
+            P._check(P.lib.pbp_simulate_point_device(ctx.handle, C.byref(cs), kind, C.c_uint64(seed), 0, chunk, snrs[0],
+                                                     0, ALPHA, max_iter, P._abi.i64p(wcnt.data_ptr()),
+                                                     C.c_void_p(stream.cuda_stream)))
+            stream.synchronize()
             for snr in snrs:
                 cnt = torch.zeros(10, dtype=torch.int64, device=dev)
                 torch.cuda.synchronize()
