@@ -77,7 +77,8 @@ template <>
 struct Cfg<14> {  // 1024 x 16: one level in shared memory, the rest in L2
     static constexpr int LOGT = 10, K = 4, MINB = 1;
     static constexpr bool r0reg = false, rx2 = false;
-    static constexpr int where(int s) { return s == 14 ? kBits : (s == 4) ? kSmem : kGlob; }
+    // L(12) joins two layouts with lane strides > 1 row (uncoalesced in L2)
+    static constexpr int where(int s) { return s == 14 ? kBits : (s == 12) ? kSmem : kGlob; }
 };
 
 template <int M_>
@@ -108,6 +109,9 @@ struct Plan {
     static constexpr int NREG = count(kReg, M + 1), NSM = count(kSmem, M + 1), NGL = count(kGlob, M + 1);
     static constexpr int pad(int row) { return row + (row >> 5); }
     static constexpr int NX = N + N / 32;
+    // L(s) is produced (stage s) and consumed (stage s-1, commits of stage
+    // s-1) in one pass layout: only its owner threads touch it
+    static constexpr bool inner(int s) { return s < M && pass_of(s) == pass_of(s - 1); }
 };
 
 __device__ __forceinline__ float xsmin(float a, float b) {
@@ -195,12 +199,20 @@ struct Dec {
         return PL::pad(j << PL::base(q));
     }
 
+    // L2-resident level index: thread-major for a level of one layout (every
+    // warp access one coalesced line per register), row-indexed otherwise
+    template <int s, int q>
+    __device__ __forceinline__ size_t gidx(int j) const {
+        if constexpr (PL::inner(s)) return ((size_t)PL::slot(s) * P + j) * kT + tid;
+        else return (size_t)PL::slot(s) * N + row<q>(j);
+    }
+
     template <int s, int q>
     __device__ __forceinline__ float ld(int j) const {
         constexpr int w = C::where(s);
         if constexpr (w == kReg) return Lr[PL::slot(s)][j];
         else if constexpr (w == kSmem) return sm->Ls[PL::slot(s)][pbase<q>() + poff<q>(j)];
-        else if constexpr (w == kGlob) return Lg[(size_t)PL::slot(s) * N + row<q>(j)];
+        else if constexpr (w == kGlob) return Lg[gidx<s, q>(j)];
         else return ((lm_nz >> j) & 1u) ? (((lm_neg >> j) & 1u) ? -kCap : kCap) : 0.f;
     }
     template <int s, int q>
@@ -208,7 +220,7 @@ struct Dec {
         constexpr int w = C::where(s);
         if constexpr (w == kReg) Lr[PL::slot(s)][j] = v;
         else if constexpr (w == kSmem) sm->Ls[PL::slot(s)][pbase<q>() + poff<q>(j)] = v;
-        else if constexpr (w == kGlob) Lg[(size_t)PL::slot(s) * N + row<q>(j)] = v;
+        else if constexpr (w == kGlob) Lg[gidx<s, q>(j)] = v;
         else {
             lm_nz |= 1u << j;
             lm_neg = v < 0.f ? (lm_neg | (1u << j)) : (lm_neg & ~(1u << j));
