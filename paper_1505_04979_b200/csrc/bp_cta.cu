@@ -5,7 +5,7 @@
 // skipped), the candidate check/commit right after each stage and the pinned
 // G-check after each sweep. What is B200-specific is where the state lives:
 //
-// * T threads own P = n/T rows each. A pass is K = log2 P consecutive stages
+// * T threads own P = n/T rows each (one frame per CTA; two CTAs per SM up to n = 4096). A pass is K = log2 P consecutive stages
 //   whose PE distances are register bits of the thread's rows, so R(s) is
 //   carried in registers from stage to stage and crosses shared memory
 //   (Rx) only between passes.
@@ -48,23 +48,14 @@ struct Cfg<11> {  // 512 threads x 4 rows, 2 CTAs per SM
     static constexpr bool r0reg = true, rx2 = true;
     static constexpr int where(int s) { return s == 11 ? kBits : (s & 1) ? kReg : kSmem; }
 };
-#ifndef PBP_CTA12_T1024
 template <>
-struct Cfg<12> {  // 512 x 8: four inner levels in registers, the other levels in shared memory
-    static constexpr int LOGT = 9, K = 3, MINB = 1;
-    static constexpr bool r0reg = true, rx2 = true;
+struct Cfg<12> {  // 256 x 16, two frames per SM: four levels in registers, five in shared memory, two in L2
+    static constexpr int LOGT = 8, K = 4, MINB = 2;
+    static constexpr bool r0reg = false, rx2 = false;
     static constexpr int where(int s) {
-        return s == 12 ? kBits : (s == 1 || s == 2 || s == 4 || s == 5) ? kReg : kSmem;
+        return s == 12 ? kBits : (s <= 3 || s == 5) ? kReg : (s == 10 || s == 11) ? kGlob : kSmem;
     }
 };
-#else
-template <>
-struct Cfg<12> {  // 1024 x 4: inner levels (odd s) in registers, boundary levels in shared memory
-    static constexpr int LOGT = 10, K = 2, MINB = 1;
-    static constexpr bool r0reg = true, rx2 = true;
-    static constexpr int where(int s) { return s == 12 ? kBits : (s & 1) ? kReg : kSmem; }
-};
-#endif
 template <>
 struct Cfg<13> {  // 1024 x 8: boundary levels in shared memory, two in registers, the rest in L2
     static constexpr int LOGT = 10, K = 3, MINB = 1;
