@@ -5,7 +5,8 @@
 // skipped), the candidate check/commit right after each stage and the pinned
 // G-check after each sweep. What is B200-specific is where the state lives:
 //
-// * T threads own P = n/T rows each (one frame per CTA; two CTAs per SM up to n = 4096). A pass is K = log2 P consecutive stages
+// * T threads own P = n/T rows each (one frame per CTA; three CTAs per SM at
+//   n = 2048, two at 4096, one beyond). A pass is K = log2 P consecutive stages
 //   whose PE distances are register bits of the thread's rows, so R(s) is
 //   carried in registers from stage to stage and crosses shared memory
 //   (Rx) only between passes.
@@ -43,10 +44,10 @@ enum : int { kReg = 0, kSmem = 1, kGlob = 2, kBits = 3 };
 template <int M>
 struct Cfg;
 template <>
-struct Cfg<11> {  // 512 threads x 4 rows, 2 CTAs per SM
-    static constexpr int LOGT = 9, K = 2, MINB = 2;
-    static constexpr bool r0reg = true, rx2 = true;
-    static constexpr int where(int s) { return s == 11 ? kBits : (s & 1) ? kReg : kSmem; }
+struct Cfg<11> {  // 256 threads x 8 rows, 3 CTAs per SM (csfg +23 % over 512 x 4 at 2 per SM)
+    static constexpr int LOGT = 8, K = 3, MINB = 3;
+    static constexpr bool r0reg = false, rx2 = false;
+    static constexpr int where(int s) { return s == 11 ? kBits : (s == 1 || s == 2 || s == 4) ? kReg : kSmem; }
 };
 template <>
 struct Cfg<12> {  // 256 x 16, two frames per SM: four levels in registers, five in shared memory, two in L2
