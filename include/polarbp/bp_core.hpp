@@ -4,8 +4,8 @@
 // double, the reference's own arithmetic (pbp_decode_trace_f64: results equal
 // the shipped reference frame by frame); decode_batch is the fp32 fast path
 // (the reference's operation order in fp32) with a double overload. pe_update
-// is kept as a host utility for the reference's known-answer tests. There is
-// no CPU decoder behind these calls.
+// and the MessageState utilities are kept as host utilities for the
+// reference's known-answer tests. There is no CPU decoder behind the decode calls.
 #include <cstdint>
 #include <span>
 #include <vector>
@@ -24,6 +24,33 @@ struct PeOutputs {
 };
 // Eq. (1) scaled min-sum update, clamped to +-LLR_CAP, sgn(0) = +1 (host utility).
 PeOutputs pe_update(const PeInputs& in, double alpha);
+
+// ---- state-level host utilities (the reference's fine-grained public API,
+// include/polarbp/bp_core.hpp:38-80, kept for its known-answer tests). The
+// decoders below never use them: they run on the GPU.
+struct MessageState {
+    int n = 0, m = 0;
+    std::vector<double> l_msg, r_msg;  // (m+1) x n each, stage-major
+
+    double& l(int stage, int row) { return l_msg[static_cast<size_t>(stage) * n + row]; }
+    const double& l(int stage, int row) const { return l_msg[static_cast<size_t>(stage) * n + row]; }
+    double& r(int stage, int row) { return r_msg[static_cast<size_t>(stage) * n + row]; }
+    const double& r(int stage, int row) const { return r_msg[static_cast<size_t>(stage) * n + row]; }
+};
+
+struct FreezeState;  // polarbp/csfg_freeze.hpp
+
+// R(0) = channel LLRs (clamped), L(m) = +LLR_CAP at frozen rows, all else 0.
+// Throws std::invalid_argument("init_state: LLR length != n").
+MessageState init_state(const PolarCode& code, std::span<const double> channel_llrs);
+// The active PEs of one stage (freeze == nullptr: all); returns how many ran.
+long long stage_pass(MessageState& state, double alpha, int stage, const FreezeState* freeze);
+// Stages 0..m-1 in order; returns the PEs executed.
+long long sweep(MessageState& state, double alpha, const FreezeState* freeze = nullptr);
+// u_hat[r] = 0 at frozen rows, else (R(m, r) < 0).
+Bits hard_output(const MessageState& state, const PolarCode& code);
+// x_hat = sign(R(0) + L(0)) equals polar_transform(hard_output).
+bool gmatrix_converged(const MessageState& state, const PolarCode& code);
 
 enum class StopReason { max_iter, gmatrix_converged, csfg_complete };
 const char* to_string(StopReason reason);

@@ -1,9 +1,11 @@
 // C++ drop-in check: the reference's unit tests (proj/tests/*.cpp, cited per
 // case) re-expressed against include/polarbp/*.hpp linked to libpbp.so.
 // Usage: test_dropin [--cpu-only]   (exit code = number of failed checks)
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -72,6 +74,113 @@ static void host_cases() {
     const auto d = freeze_decision(std::vector<double>{-3.0, -1.0, -2.0, -4.0}, fr);
     CHECK(d.has_value() && d->u_hat == (Bits{0, 0, 0, 1}));
     CHECK(!freeze_decision(std::vector<double>{-3.0, 1.0, 2.0, 4.0}, fr).has_value());
+    // state-level host utilities (test_bp_core.cpp:102-183)
+    {
+        const std::vector<double> llrs{1, -2, 3, -4, 5, -6, 7, -8};
+        const MessageState st = init_state(c84, llrs);
+        bool ok = true;
+        for (int r = 0; r < 8; ++r) {
+            ok = ok && st.r(0, r) == llrs[r] && st.l(3, r) == (c84.frozen[r] ? LLR_CAP : 0.0);
+            for (int s2 = 1; s2 <= 3; ++s2) ok = ok && st.r(s2, r) == 0.0;
+            for (int s2 = 0; s2 < 3; ++s2) ok = ok && st.l(s2, r) == 0.0;
+        }
+        CHECK(ok);
+        CHECK(throws([&] { init_state(c84, std::vector<double>(7, 0.0)); }));
+        MessageState s1 = init_state(c84, std::vector<double>(8, 1.0));
+        CHECK(sweep(s1, 0.9375) == 12);
+        std::mt19937_64 gen(8103);
+        std::uniform_real_distribution<double> uni(-5.0, 5.0);
+        std::vector<double> rnd(8);
+        for (double& v : rnd) v = uni(gen);
+        MessageState s2 = init_state(c84, rnd);
+        FreezeState all(8);
+        all.freeze_stage.assign(8, -1);  // below every stage: no PE active
+        const MessageState before = s2;
+        CHECK(sweep(s2, 0.9375, &all) == 0 && s2.l_msg == before.l_msg && s2.r_msg == before.r_msg);
+        const PolarCode c32 = PolarCode::construct(32, 16, 0.5);
+        std::vector<double> r32(32);
+        for (double& v : r32) v = uni(gen);
+        MessageState s3 = init_state(c32, r32);
+        const std::vector<double> lb = s3.l_msg;
+        for (int t = 0; t < 5; ++t) sweep(s3, 0.9375);
+        ok = true;
+        for (int r = 0; r < 32; ++r) ok = ok && s3.r(0, r) == r32[r] && s3.l(c32.m, r) == lb[5 * 32 + r];
+        CHECK(ok);
+        MessageState s4 = init_state(c84, std::vector<double>(8, 2.0));
+        sweep(s4, 0.9375);
+        ok = true;
+        for (int r = 0; r < 8; ++r) ok = ok && s4.r(3, r) > 0.0;
+        CHECK(ok && hard_output(s4, c84) == Bits(8, 0));
+        MessageState s5 = init_state(c84, std::vector<double>(8, 1.0));
+        for (int r = 0; r < 8; ++r) s5.r(3, r) = 1.0;
+        s5.r(3, 3) = -0.1;
+        CHECK(hard_output(s5, c84) == (Bits{0, 0, 0, 1, 0, 0, 0, 0}));
+        s5.r(3, 3) = 0.0;  // a tie decides 0
+        CHECK(hard_output(s5, c84) == Bits(8, 0));
+        s5.r(3, 0) = -9.0;  // frozen rows stay 0
+        CHECK(hard_output(s5, c84) == Bits(8, 0));
+        const PolarCode c22 = PolarCode::construct(2, 2, 0.5);
+        CHECK(gmatrix_converged(init_state(c22, std::vector<double>{1.0, 1.0}), c22));
+        CHECK(!gmatrix_converged(init_state(c22, std::vector<double>{-1.0, 1.0}), c22));
+    }
+    // FreezeState, apply_freeze, is_pe_active, mld_oracle (test_csfg_freeze.cpp:100-220)
+    {
+        MessageState st = init_state(c84, std::vector<double>(8, 1.0));
+        FreezeState fz(8);
+        apply_freeze(st, fz, BlockRef{1, 0, 0, 2}, {{1, 0}, {1, 1}}, 1);
+        CHECK(fz.frontier == 2 && st.l(2, 0) == -LLR_CAP && st.l(2, 1) == LLR_CAP && fz.freeze_stage[0] == 1 &&
+              fz.decided_u[0] == 1 && fz.decided_u[1] == 1);
+        apply_freeze(st, fz, BlockRef{0, 0, 0, 4}, {{0, 0, 0, 0}, {0, 0, 0, 0}}, 2);  // the enclosing block supersedes
+        bool ok = fz.frontier == 4;
+        for (int r = 0; r < 4; ++r) ok = ok && st.l(1, r) == LLR_CAP && fz.freeze_stage[r] == 0 && fz.decided_u[r] == 0;
+        CHECK(ok && fz.events.size() == 2 && fz.events[1].iteration == 2);
+        CHECK(candidate_block(fz, 1).start == 4 && candidate_block(fz, 1).size == 2 && candidate_block(fz, 1).index == 2);
+        auto count_active = [&](const FreezeState& f) {
+            int a = 0;
+            for (int s2 = 0; s2 < c84.m; ++s2)
+                for (int r = 0; r < 8; ++r)
+                    if (!(r & (8 >> (s2 + 1))) && is_pe_active(f, s2, r)) ++a;
+            return a;
+        };
+        FreezeState f0(8);
+        CHECK(count_active(f0) == 12);
+        FreezeState f1(8);
+        for (int r = 0; r < 4; ++r) f1.freeze_stage[r] = 0;
+        CHECK(count_active(f1) == 8 && is_pe_active(f1, 0, 0) && !is_pe_active(f1, 1, 0) && !is_pe_active(f1, 2, 2));
+        FreezeState f2(8);
+        f2.freeze_stage[0] = f2.freeze_stage[1] = 1;
+        CHECK(count_active(f2) == 11 && !is_pe_active(f2, 2, 0) && is_pe_active(f2, 1, 0));
+        CHECK(mld_oracle(std::vector<double>{3.0, 1.0, 2.0, 4.0}, Bits{1, 1, 1, 0}) == Bits(4, 0));
+        CHECK(throws([] { mld_oracle(std::vector<double>(16, 1.0), Bits(16, 0), 8); }));
+        // freeze_decision accepts exactly when it equals the block ML decision
+        std::mt19937_64 gen(9002);
+        std::uniform_real_distribution<double> uni(-5.0, 5.0);
+        int accepted = 0, agree = 0;
+        for (int rep = 0; rep < 1000; ++rep) {
+            const int len = 2 << (gen() % 4);
+            std::vector<double> r(len);
+            for (double& v : r)
+                do v = uni(gen);
+                while (v == 0.0);
+            Bits fr(len);
+            for (auto& f : fr) f = gen() & 1;
+            const Bits ml = mld_oracle(r, fr);
+            const auto dec = freeze_decision(r, fr);
+            double abs_sum = 0.0, ml_score = 0.0;
+            const Bits xm = polar_transform(ml);
+            for (int i = 0; i < len; ++i) {
+                abs_sum += std::fabs(r[i]);
+                ml_score += xm[i] ? -r[i] : r[i];
+            }
+            if (dec) {
+                ++accepted;
+                agree += dec->u_hat == ml;
+            } else {
+                agree += ml_score < abs_sum;
+            }
+        }
+        CHECK(agree == 1000 && accepted > 50);
+    }
     // results CSV round trip + savings (test_sim_harness.cpp:93-182)
     std::vector<PointStats> rows(3);
     for (int i = 0; i < 3; ++i) {
@@ -101,6 +210,48 @@ static void gpu_cases() {
     o = decode_csfg(c84, fives, 0.9375, 40, &ev);
     CHECK(o.iterations_used == 1 && o.pe_activations == 7);
     CHECK(ev.size() == 3 && ev[0].stage == 0 && ev[0].size == 4 && ev[1].start == 4 && ev[2].start == 6);
+    // test_csfg_freeze.cpp:248-293: 300 trials of (64,32) at 2 dB, seed 4242: the
+    // frontier grows as a prefix, stamps increase, and replaying the GPU's freeze
+    // events through FreezeState/is_pe_active reproduces its PE count
+    {
+        const PolarCode c64 = PolarCode::construct(64, 32, 0.5);
+        int bad = 0;
+        for (int t = 0; t < 300; ++t) {
+            TrialRng rng(4242, t);
+            Bits info(32);
+            for (auto& b : info) b = rng.bit();
+            const auto llr = transmit_awgn(modulate_bpsk(encode(c64, info).x), {2.0, 0.5, false}, rng);
+            std::vector<FreezeEvent> evs;
+            const DecodeOutcome out = decode_csfg(c64, llr, 0.9375, 40, &evs);
+            for (int i : c64.frozen_positions()) bad += out.u_hat[i] != 0;
+            int frontier = 0;
+            for (size_t e = 0; e < evs.size(); ++e) {
+                const FreezeEvent& ev = evs[e];
+                bad += !(ev.start <= frontier && ev.start + ev.size > frontier && ev.start % ev.size == 0 &&
+                         ev.size == 64 >> (ev.stage + 1));
+                if (e) bad += !(ev.iteration > evs[e - 1].iteration ||
+                                (ev.iteration == evs[e - 1].iteration && ev.stage > evs[e - 1].stage));
+                frontier = ev.start + ev.size;
+            }
+            bad += (out.stop_reason == StopReason::csfg_complete) != (frontier == 64);
+            FreezeState fz(64);
+            long long pe = 0;
+            size_t e = 0;
+            for (int it = 1; it <= out.iterations_used; ++it)
+                for (int s2 = 0; s2 < c64.m && fz.frontier < 64; ++s2) {
+                    for (int r = 0; r < 64; ++r)
+                        if (!(r & (64 >> (s2 + 1))) && is_pe_active(fz, s2, r)) ++pe;
+                    if (e < evs.size() && evs[e].iteration == it && evs[e].stage == s2) {
+                        for (int r = evs[e].start; r < evs[e].start + evs[e].size; ++r)
+                            fz.freeze_stage[r] = std::min(fz.freeze_stage[r], s2);
+                        fz.frontier = evs[e].start + evs[e].size;
+                        ++e;
+                    }
+                }
+            bad += pe != out.pe_activations;
+        }
+        CHECK(bad == 0);
+    }
     // test_bp_core.cpp:206-227: 6 dB, (64,32), seed 99: <= 2 wrong of 50
     const PolarCode c64 = PolarCode::construct(64, 32, 0.5);
     int wrong = 0;
