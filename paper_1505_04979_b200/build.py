@@ -40,11 +40,24 @@ def _sources():
     return cu, cpp, deps
 
 
-def _stale(obj, src, deps):
-    if not os.path.exists(obj):
+def _stale(obj, src, deps, flags):
+    """Rebuild when a source or header is newer, or the compile command changed
+    (a .flags stamp next to the object records the flags it was built with)."""
+    stamp = obj + ".flags"
+    if not os.path.exists(obj) or not os.path.exists(stamp):
         return True
+    with open(stamp) as f:
+        if f.read() != " ".join(flags):
+            return True
     t = os.path.getmtime(obj)
     return any(os.path.getmtime(p) > t for p in [src] + deps)
+
+
+def _stamp(cmd):
+    obj = cmd[cmd.index("-o") + 1]
+    flags = cmd[1:cmd.index("-c")]
+    with open(obj + ".flags", "w") as f:
+        f.write(" ".join(flags))
 
 
 def build(verbose=False, jobs=None):
@@ -55,12 +68,12 @@ def build(verbose=False, jobs=None):
     for f in cu:
         src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
         objs.append(obj)
-        if _stale(obj, src, deps):
+        if _stale(obj, src, deps, NVFLAGS):
             cmds.append([NVCC] + NVFLAGS + ["-c", src, "-o", obj])
     for f in cpp:
         src, obj = os.path.join(CSRC, f), os.path.join(OBJ, f + ".o")
         objs.append(obj)
-        if _stale(obj, src, deps):
+        if _stale(obj, src, deps, CXXFLAGS):
             cmds.append(["g++"] + CXXFLAGS + ["-c", src, "-o", obj])
     procs = []
     for c in cmds:
@@ -73,8 +86,10 @@ def build(verbose=False, jobs=None):
         if p.returncode != 0:
             failed = True
             sys.stderr.write(out)
-        elif verbose and out.strip():
-            print(out)
+        else:
+            _stamp(c)
+            if verbose and out.strip():
+                print(out)
     if failed:
         raise RuntimeError("libpbp build failed")
     if cmds or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
