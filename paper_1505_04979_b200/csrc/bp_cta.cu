@@ -467,11 +467,23 @@ struct Dec {
         const uint32_t u = (uint32_t)(W >> (i * P));
         const uint32_t x = (uint32_t)(snap >> (i * P));
         if (bm) {
+            // L(S+1) = +-CAP: register levels by compile-time index, L(m) as
+            // masks, the rest in the runtime loop below (commits are rare: the
+            // loop keeps their code small in the instruction cache)
+            constexpr int wl = C::where(S + 1);
+            if constexpr (wl == kReg) {
 #pragma unroll
-            for (int j = 0; j < P; ++j) {
-                if (!((bm >> j) & 1u)) continue;
+                for (int j = 0; j < P; ++j)
+                    if ((bm >> j) & 1u) Lr[PL::slot(S + 1)][j] = ((x >> j) & 1u) ? -kCap : kCap;
+            } else if constexpr (wl == kBits) {
+                lm_nz |= bm;
+                lm_neg = (lm_neg & ~bm) | (x & bm);
+            }
+#pragma unroll 1
+            for (uint32_t left = bm; left; left &= left - 1u) {
+                const int j = __ffs(left) - 1;
                 const int r = row<q>(j);
-                st<S + 1, q>(j, ((x >> j) & 1u) ? -kCap : kCap);
+                if constexpr (wl == kSmem || wl == kGlob) st<S + 1, q>(j, ((x >> j) & 1u) ? -kCap : kCap);
                 if ((int)sm->fst[r] > S) sm->fst[r] = (uint8_t)S;
                 const uint32_t bit = 1u << (r & 31);
                 if ((u >> j) & 1u) atomicOr(&sm->dec[r >> 5], bit);
