@@ -507,14 +507,11 @@ struct Dec {
     __device__ __forceinline__ void uncount(uint32_t bm, bool all) {
         constexpr int S = q * K + i;
         if constexpr (S <= PL::last(q)) {
-            constexpr int dj = 1 << (M - 1 - S - PL::base(q));
-            uint32_t tm = 0u;  // top rows of stage S inside the block, as PE indices
-#pragma unroll
-            for (int j = 0, k = 0; j < P; ++j) {
-                if (j & dj) continue;
-                tm |= ((bm >> j) & 1u) << k;
-                ++k;
-            }
+            // top rows of stage S inside the block, as PE indices: the block is
+            // the register run [j0, j0 + n) (n a power of two larger than the
+            // stage's register distance), so its top rows are the PE run
+            // [j0 / 2, j0 / 2 + n / 2)
+            const uint32_t tm = bm ? low_mask(__popc(bm) >> 1) << ((__ffs(bm) - 1) >> 1) : 0u;
             const uint32_t drop = (all ? low_mask(P / 2) : tm) << (i * (P / 2)) & onm;
             act -= __popc(drop);
             onm &= ~drop;
