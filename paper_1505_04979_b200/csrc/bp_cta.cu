@@ -58,11 +58,11 @@ struct Cfg<12> {  // 256 x 16, two frames per SM: four levels in registers, five
     }
 };
 template <>
-struct Cfg<13> {  // 1024 x 8: boundary levels in shared memory, two in registers, the rest in L2
-    static constexpr int LOGT = 10, K = 3, MINB = 1;
-    static constexpr bool r0reg = false, rx2 = true;
+struct Cfg<13> {  // 512 x 16: three levels in registers, five in shared memory, four in L2
+    static constexpr int LOGT = 9, K = 4, MINB = 1;
+    static constexpr bool r0reg = false, rx2 = false;
     static constexpr int where(int s) {
-        return s == 13 ? kBits : (s % 3 == 0) ? kSmem : (s <= 2) ? kReg : kGlob;
+        return s == 13 ? kBits : (s <= 3) ? kReg : (s % 4 == 0 || s == 5 || s == 6) ? kSmem : kGlob;
     }
 };
 template <>
