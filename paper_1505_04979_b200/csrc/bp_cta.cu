@@ -1,9 +1,10 @@
 // CTA-per-frame BP decoder for n = 2048 .. 16384 (configs 3 and 4).
 //
-// The reference schedule literally (src/bp_core.cpp:58-86, csfg_freeze.cpp:
-// 99-152): every stage's PEs under the is_pe_active mask (inactive PEs are
-// skipped), the candidate check/commit right after each stage and the pinned
-// G-check after each sweep. What is B200-specific is where the state lives:
+// The reference schedule (src/bp_core.cpp:58-86, csfg_freeze.cpp:99-152):
+// every stage's PEs under the is_pe_active mask (inactive PEs keep their
+// state), at most one candidate check/commit per stage in stage order, and
+// the pinned G-check after each sweep. What is B200-specific is where the
+// state lives and when the checks run:
 //
 // * T threads own P = n/T rows each (one frame per CTA; three CTAs per SM at
 //   n = 2048, two at 4096, one beyond). A pass is K = log2 P consecutive stages
@@ -12,16 +13,21 @@
 //   (Rx) only between passes.
 // * L(s) for a stage s inside a pass is produced and consumed by the same
 //   thread (stage s writes it, stage s-1 reads it, both in the pass's row
-//   layout): those levels live in registers. Levels at pass boundaries are
-//   exchanged between layouts in shared memory (or L2 for n >= 8192, where
-//   shared memory runs out); L(m) in {0, +-CAP} is two bit masks.
-// * The candidate check (polar transform of the block's hard decisions,
-//   csfg_freeze.cpp:18-39) and the G-check transform run where the bits are:
-//   the row bits held in a thread's registers in-thread, lane bits by
-//   shuffles, warp bits by one shared-memory superset XOR, and the verdict by
-//   __syncthreads_or: one or two barriers per stage. A commit
-//   (apply_freeze, csfg_freeze.cpp:82-93) is applied by the owners of the
-//   block's rows; frontier and event count are kept uniformly in registers.
+//   layout): those levels live in registers, or where registers run out in
+//   shared memory or as thread-major (coalesced) L2 arrays. Levels at pass
+//   boundaries are exchanged between layouts in row-indexed shared memory
+//   (L2 for some at n >= 8192); L(m) in {0, +-CAP} is two bit masks.
+// * csfg checks are deferred to the end of each pass: its stages run as if
+//   none of its checks commits; then one batched polar transform of the
+//   stages' hard decisions (csfg_freeze.cpp:18-39: register bits in-thread,
+//   lane bits by shuffles, warp bits by one shared-memory superset XOR) and
+//   one OR-reduction decide every candidate for every frontier an earlier
+//   commit of the pass can produce, and the commits (apply_freeze,
+//   csfg_freeze.cpp:82-93) are applied in stage order by the owners of the
+//   block's rows, with the PE count corrected for the PEs the reference
+//   would have skipped. Rows of a committed block pair only with each other
+//   at later stages, so their speculative values are never observed.
+//   Frontier and event count are uniform registers.
 //
 // Arithmetic as in the warp-resident kernel (one min.xorsign.abs per
 // min-with-sign, every product and sum rounded on its own, r_top =
