@@ -380,7 +380,7 @@ def test_cta_kernel_reroute_and_events(ctx):
     llr[4, :] *= 1e25
     exp = O.decode_batch("csfg", fz, llr, 0.9375, 40, prec=32)
     got = P.decode_batch(code, "csfg", llr, 0.9375, 40, ctx=ctx)
-    assert ctx.last_launch_info()[1] == 2
+    assert ctx.last_launch_info()[1] == 2  # frames 1 and 4 went to the generic kernel
     assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"])
     for f in ("iterations", "pe", "stop", "n_events"):
         assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), f
@@ -391,3 +391,24 @@ def test_cta_kernel_reroute_and_events(ctx):
         got_ev = np.array([[x.iteration, x.stage, x.block, x.start, x.size] for x in events], np.int64)
         assert np.array_equal(got_ev.reshape(-1, 5), np.asarray(e["events"], np.int64).reshape(-1, 5)), i
         assert out.pe_activations == e["pe"] and out.iterations_used == e["iterations"], i
+
+
+@pytest.mark.parametrize("n", [2048, 4096, 8192, 16384])
+@pytest.mark.parametrize("kind", ["gmatrix", "csfg"])
+@pytest.mark.parametrize("rate", [0.25, 0.875])
+def test_cta_kernel_random_frozen_sets(ctx, n, kind, rate):
+    """The CTA-per-frame kernel on random frozen sets and channel-like LLRs at several
+    SNRs (commit patterns of every stage of a pass, re-covered rows, early G-stops)."""
+    rng = np.random.default_rng(int(9000 * rate) + n + len(kind))
+    k = max(1, int(n * rate))
+    fz = _random_frozen(rng, n, k)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    frames = 12 if n <= 4096 else 6
+    scale = rng.choice([2.0, 4.0, 8.0, 16.0], size=(frames, 1))
+    llr = (scale * (1.0 + rng.normal(0.0, 1.0, size=(frames, n)))).astype(np.float32)
+    exp = O.decode_batch(kind, fz, llr, 0.9375, 30, prec=32)
+    assert P.lib.pbp_kernel_path(n) == 2
+    got = P.decode_batch(code, kind, llr, 0.9375, 30, ctx=ctx)
+    assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"])
+    for f in ("iterations", "pe", "stop", "n_events"):
+        assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), f
