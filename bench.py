@@ -335,11 +335,20 @@ def main():
         # the whole sweep (every Eb/N0 point's frames) in one host-buffer call;
         # if that much host memory cannot be pinned, the 3 dB point alone
         try:
+            host_llr = torch.empty((len(SNRS) * frames, N), dtype=torch.float32, pin_memory=True)
+            whole = 1
+        except RuntimeError:
+            host_llr, whole = None, 0
+        if dist:  # every rank times the same scope
+            flag = torch.tensor([whole], device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            whole = int(flag.item())
+        if whole:
             nb = len(SNRS) * frames
-            host_llr = torch.empty((nb, N), dtype=torch.float32, pin_memory=True)
             host_llr.copy_(llr.reshape(nb, N))
             e2e_scope = f"the sweep's {nb} frames/GPU"
-        except RuntimeError:
+        else:
+            del host_llr
             nb = frames
             host_llr = torch.empty((nb, N), dtype=torch.float32, pin_memory=True)
             host_llr.copy_(llr[SNRS.index(3.0)])
