@@ -68,6 +68,37 @@ static void host_cases() {
     const PeOutputs p = pe_update({2.0, -3.0, 1.0, 0.5}, 0.9375);
     CHECK(p.l_top == -1.875 && p.r_bot == 1.4375);
     CHECK(pe_update({LLR_CAP, LLR_CAP, LLR_CAP, LLR_CAP}, 1.0).l_bot == LLR_CAP);
+    // test_bp_core.cpp:39-91: zero counts as positive; flipping the wire signs along a
+    // codeword of the PE's check negates exactly the messages on the flipped wires;
+    // scaling shrinks the two pure-product outputs
+    {
+        const PeOutputs z = pe_update({0.0, 2.0, 3.0, 1.0}, 1.0);
+        CHECK(z.l_top == 0.0 && z.r_bot == 1.0 && z.r_top == 3.0);
+        std::mt19937_64 gen(8101);
+        std::uniform_real_distribution<double> uni(-20.0, 20.0);
+        const int pat[3][3] = {{1, 1, 0}, {1, 0, 1}, {0, 1, 1}};  // flips of wires a, c, b
+        int bad = 0;
+        for (int rep = 0; rep < 10000; ++rep) {
+            const PeInputs in{uni(gen), uni(gen), uni(gen), uni(gen)};
+            if (in.l_top == 0.0 || in.l_bot == 0.0 || in.r_top == 0.0 || in.r_bot == 0.0) continue;
+            const PeOutputs base = pe_update(in, 0.9375);
+            for (const auto& f : pat) {
+                const double fa = f[0] ? -1.0 : 1.0, fc = f[1] ? -1.0 : 1.0, fb = f[2] ? -1.0 : 1.0;
+                const PeOutputs o = pe_update({fc * in.l_top, fb * in.l_bot, fa * in.r_top, fb * in.r_bot}, 0.9375);
+                bad += !(o.l_top == fa * base.l_top && o.l_bot == fb * base.l_bot && o.r_top == fc * base.r_top &&
+                         o.r_bot == fb * base.r_bot);
+            }
+        }
+        CHECK(bad == 0);
+        std::mt19937_64 g2(8102);
+        bad = 0;
+        for (int rep = 0; rep < 2000; ++rep) {
+            const PeInputs in{uni(g2), uni(g2), uni(g2), uni(g2)};
+            const PeOutputs h = pe_update(in, 0.5), f = pe_update(in, 1.0);
+            bad += !(std::fabs(h.l_top) <= std::fabs(f.l_top) + 1e-12 && std::fabs(h.r_top) <= std::fabs(f.r_top) + 1e-12);
+        }
+        CHECK(bad == 0);
+    }
     // test_csfg_freeze.cpp:51-97
     CHECK(candidate_block(8, 4, 1).start == 4 && candidate_block(8, 4, 1).size == 2);
     const std::vector<std::uint8_t> fr(c84.frozen.begin(), c84.frozen.begin() + 4);
@@ -251,6 +282,26 @@ static void gpu_cases() {
             bad += pe != out.pe_activations;
         }
         CHECK(bad == 0);
+    }
+    // test_csfg_freeze.cpp:295-314: past the frontier, decode_csfg falls back to the hard
+    // decisions (0 dB, two iterations: some frame stops at max_iter with frozen rows 0)
+    {
+        const PolarCode c64 = PolarCode::construct(64, 32, 0.5);
+        bool saw = false;
+        int bad = 0;
+        for (int t = 0; t < 50 && !saw; ++t) {
+            TrialRng rng(777, t);
+            Bits info(32);
+            for (auto& b : info) b = rng.bit();
+            const auto llr = transmit_awgn(modulate_bpsk(encode(c64, info).x), {0.0, 0.5, false}, rng);
+            const DecodeOutcome out = decode_csfg(c64, llr, 0.9375, 2);
+            if (out.stop_reason == StopReason::max_iter) {
+                saw = true;
+                bad += out.iterations_used != 2;
+                for (int i : c64.frozen_positions()) bad += out.u_hat[i] != 0;
+            }
+        }
+        CHECK(saw && bad == 0);
     }
     // test_bp_core.cpp:206-227: 6 dB, (64,32), seed 99: <= 2 wrong of 50
     const PolarCode c64 = PolarCode::construct(64, 32, 0.5);
