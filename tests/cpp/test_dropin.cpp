@@ -212,6 +212,17 @@ static void host_cases() {
         }
         CHECK(agree == 1000 && accepted > 50);
     }
+    // acceptance.cpp:302-309: the polar transform is an involution
+    {
+        std::mt19937_64 gen(9006);
+        int bad = 0;
+        for (int rep = 0; rep < 10000; ++rep) {
+            Bits u(1u << (gen() % 11));
+            for (auto& b : u) b = static_cast<std::uint8_t>(gen() >> 63);
+            bad += polar_transform(polar_transform(u)) != u;
+        }
+        CHECK(bad == 0);
+    }
     // results CSV round trip + savings (test_sim_harness.cpp:93-182)
     std::vector<PointStats> rows(3);
     for (int i = 0; i < 3; ++i) {
@@ -302,6 +313,74 @@ static void gpu_cases() {
             }
         }
         CHECK(saw && bad == 0);
+    }
+    // acceptance.cpp:209-272, 275-300 (criterion 6): 10^4 random small codes, lengths,
+    // rates, design points, iteration caps and Eb/N0 - frozen-bit safety of csfg and
+    // G-stop, prefix-only frontier growth with increasing (iteration, stage) stamps,
+    // per-iteration activation counts that never increase, and the replayed total equal
+    // to the reported PE count (the decided-prefix part needs FreezeEvent::x_hat, which
+    // the GPU trace does not carry)
+    {
+        std::mt19937_64 gen(9006);
+        std::uniform_real_distribution<double> unif(0.0, 1.0);
+        long long frozen_bad = 0, frontier_bad = 0, mono_bad = 0;
+        for (int rep = 0; rep < 10000; ++rep) {
+            const int m = 2 + static_cast<int>(gen() % 5);
+            const int n = 1 << m;
+            const int k = 1 + static_cast<int>(gen() % n);
+            const PolarCode code = PolarCode::construct(n, k, 0.25 + 0.5 * unif(gen));
+            const int max_iter = 4 + static_cast<int>(gen() % 12);
+            const double snr = 4.0 * unif(gen);
+            TrialRng rng(9006, static_cast<std::uint64_t>(rep));
+            Bits info(code.k);
+            for (auto& b : info) b = rng.bit();
+            const auto llr = transmit_awgn(modulate_bpsk(encode(code, info).x),
+                                           {snr, static_cast<double>(code.k) / n, false}, rng);
+            std::vector<FreezeEvent> evs;
+            const DecodeOutcome oc = decode_csfg(code, llr, 0.9375, max_iter, &evs);
+            const DecodeOutcome og = decode_gmatrix(code, llr, 0.9375, max_iter);
+            for (int r = 0; r < n; ++r)
+                if (code.frozen[r] && (oc.u_hat[r] || og.u_hat[r])) {
+                    ++frozen_bad;
+                    break;
+                }
+            long long f = 0;
+            int pi = 0, ps = 0;
+            bool ok = true;
+            for (const FreezeEvent& ev : evs) {
+                const int size = n >> (ev.stage + 1);
+                ok = ok && ev.size == size && size > 0 && ev.start % size == 0 && ev.block == ev.start / size &&
+                     ev.start <= f && ev.start + ev.size > f &&
+                     (ev.iteration > pi || (ev.iteration == pi && ev.stage > ps));
+                pi = ev.iteration;
+                ps = ev.stage;
+                f = ev.start + ev.size;
+            }
+            ok = ok && (oc.stop_reason == StopReason::csfg_complete) == (f == n);
+            frontier_bad += !ok;
+            FreezeState fz(n);
+            long long total = 0, prev = -1;
+            size_t e = 0;
+            bool mono = true;
+            for (int t = 1; t <= oc.iterations_used && fz.frontier < n; ++t) {
+                long long cnt = 0;
+                for (int s2 = 0; s2 < m && fz.frontier < n; ++s2) {
+                    for (int r = 0; r < n; ++r)
+                        if (!(r & (n >> (s2 + 1))) && is_pe_active(fz, s2, r)) ++cnt;
+                    while (e < evs.size() && evs[e].iteration == t && evs[e].stage == s2) {
+                        for (int r = evs[e].start; r < evs[e].start + evs[e].size; ++r)
+                            fz.freeze_stage[r] = std::min(fz.freeze_stage[r], s2);
+                        fz.frontier = evs[e].start + evs[e].size;
+                        ++e;
+                    }
+                }
+                total += cnt;
+                mono = mono && (prev < 0 || cnt <= prev);
+                prev = cnt;
+            }
+            mono_bad += !(mono && total == oc.pe_activations && e == evs.size());
+        }
+        CHECK(frozen_bad == 0 && frontier_bad == 0 && mono_bad == 0);
     }
     // test_bp_core.cpp:206-227: 6 dB, (64,32), seed 99: <= 2 wrong of 50
     const PolarCode c64 = PolarCode::construct(64, 32, 0.5);
