@@ -131,6 +131,14 @@ int pbp_decode_trace(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
                      float alpha, int32_t max_iter, uint8_t* u_hat, int32_t* iterations,
                      int64_t* pe, int32_t* stop, int32_t* n_events, int32_t* events,
                      int32_t events_cap);
+/* As pbp_decode_trace, plus FreezeEvent::x_hat (csfg_freeze.hpp:34): events_xhat
+ * receives events_cap x ceil(n/32) words; event e's block decisions (the hard
+ * decision of R(stage+1) at commit time) are bits start..start+size-1 of its
+ * row-order word vector, every other bit 0. */
+int pbp_decode_trace_x(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs,
+                       float alpha, int32_t max_iter, uint8_t* u_hat, int32_t* iterations,
+                       int64_t* pe, int32_t* stop, int32_t* n_events, int32_t* events,
+                       int32_t events_cap, uint32_t* events_xhat);
 
 /* ---- fp64: the reference as shipped --------------------------------------
  * Same calls with double LLRs and alpha, decoded in double in the reference's
@@ -146,6 +154,10 @@ int pbp_decode_trace_f64(pbp_ctx* ctx, const pbp_code* code, int decoder, const 
                          double alpha, int32_t max_iter, uint8_t* u_hat, int32_t* iterations,
                          int64_t* pe, int32_t* stop, int32_t* n_events, int32_t* events,
                          int32_t events_cap);
+int pbp_decode_trace_f64_x(pbp_ctx* ctx, const pbp_code* code, int decoder, const double* llrs,
+                           double alpha, int32_t max_iter, uint8_t* u_hat, int32_t* iterations,
+                           int64_t* pe, int32_t* stop, int32_t* n_events, int32_t* events,
+                           int32_t events_cap, uint32_t* events_xhat);
 /* run_point's counters with the reference's double LLRs (src/sim_harness.cpp:67-73). */
 int pbp_simulate_point_f64(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed,
                            int64_t first_trial, int64_t frames, double ebn0_db, int noiseless,

@@ -230,12 +230,13 @@ def device_count() -> int:
 
 @dataclass
 class FreezeEvent:
-    """FreezeEvent (csfg_freeze.hpp:28-35); x_hat is not carried by the GPU trace."""
+    """FreezeEvent (csfg_freeze.hpp:28-35): x_hat = the block's hard decisions at freeze time."""
     iteration: int
     stage: int
     block: int
     start: int
     size: int
+    x_hat: Optional[np.ndarray] = None
 
 
 @dataclass
@@ -320,13 +321,18 @@ def _decode_one(code: PolarCode, kind: int, llrs, alpha, max_iter, events=None, 
     it, sp, ne = C.c_int32(), C.c_int32(), C.c_int32()
     pe = C.c_int64()
     cs = code.c_struct()
-    fn, lp = (lib.pbp_decode_trace_f64, _abi.f64p(llr)) if f64 else (lib.pbp_decode_trace, _abi.f32p(llr))
+    nw = (code.n + 31) // 32
+    xw = np.zeros(cap * nw if events is not None else 1, np.uint32)  # each event's x_hat
+    xp = xw.ctypes.data_as(C.POINTER(C.c_uint32)) if events is not None else None
+    fn, lp = (lib.pbp_decode_trace_f64_x, _abi.f64p(llr)) if f64 else (lib.pbp_decode_trace_x, _abi.f32p(llr))
     _check(fn(ctx.handle, C.byref(cs), kind, lp, float(alpha), int(max_iter), _abi.u8p(u), C.byref(it),
-              C.byref(pe), C.byref(sp), C.byref(ne), _abi.i32p(ev), cap))
+              C.byref(pe), C.byref(sp), C.byref(ne), _abi.i32p(ev), cap, xp))
     if events is not None:
         events.clear()
         for i in range(min(ne.value, cap)):
-            events.append(FreezeEvent(*[int(x) for x in ev[5 * i: 5 * i + 5]]))
+            it_, st_, bl_, sa_, sz_ = (int(x) for x in ev[5 * i: 5 * i + 5])
+            bits = unpack_bits(xw[i * nw:(i + 1) * nw], code.n)[sa_:sa_ + sz_].copy()
+            events.append(FreezeEvent(it_, st_, bl_, sa_, sz_, bits))
     return DecodeOutcome(u, extract_info_bits(code, u), it.value, pe.value, sp.value, ne.value)
 
 

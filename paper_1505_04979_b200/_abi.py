@@ -65,6 +65,14 @@ SIGNATURES = {
                                    C.POINTER(C.c_uint8), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                    C.c_int32]),
+    "pbp_decode_trace_x": (C.c_int, [_P, _CP, C.c_int, C.POINTER(C.c_float), C.c_float, C.c_int32,
+                                     C.POINTER(C.c_uint8), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                     C.c_int32, C.POINTER(C.c_uint32)]),
+    "pbp_decode_trace_f64_x": (C.c_int, [_P, _CP, C.c_int, C.POINTER(C.c_double), C.c_double, C.c_int32,
+                                         C.POINTER(C.c_uint8), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                         C.c_int32, C.POINTER(C.c_uint32)]),
     "pbp_decode_batch_f64": (C.c_int, [_P, _CP, C.c_int, C.POINTER(C.c_double), C.c_int64, C.c_double,
                                        C.c_int32, C.POINTER(PbpFrameOut)]),
     "pbp_decode_batch_f64_device": (C.c_int, [_P, _CP, C.c_int, C.POINTER(C.c_double), C.c_int64,

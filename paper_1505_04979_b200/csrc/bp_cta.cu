@@ -494,6 +494,8 @@ struct Dec {
                 const uint32_t bit = 1u << (r & 31);
                 if ((u >> j) & 1u) atomicOr(&sm->dec[r >> 5], bit);
                 else atomicAnd(&sm->dec[r >> 5], ~bit);
+                if (a->ev_xhat && nev < a->ev_cap && ((x >> j) & 1u))
+                    atomicOr(&a->ev_xhat[((long long)sm->frame * a->ev_cap + nev) * NW + (r >> 5)], bit);
             }
         }
         if (tid == 0 && a->events && nev < a->ev_cap) {

@@ -244,6 +244,8 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
                         const int r = start + i;
                         L[(size_t)s * n + r] = (R[r] < T(0)) ? -cap : cap;  // L(s+1)
                         if ((int)fst[r] > s) fst[r] = (uint8_t)s;
+                        if (a.ev_xhat && s_nev < a.ev_cap && R[r] < T(0))
+                            atomicOr(&a.ev_xhat[((size_t)frame * a.ev_cap + s_nev) * nw_all + (r >> 5)], 1u << (r & 31));
                     }
                     if (sz >= 32) {
                         for (int q = tid; q < nw; q += BLOCK) dec_u[(start >> 5) + q] = wb0[q];

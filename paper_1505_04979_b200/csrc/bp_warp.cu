@@ -823,6 +823,8 @@ struct Dec {
                 e[3] = start;
                 e[4] = sz;
             }
+            if (a->ev_xhat && nev < a->ev_cap)  // FreezeEvent::x_hat (trace calls only)
+                scatter(a->ev_xhat + ((long long)frame_ * a->ev_cap + nev) * NW, xbits, in_block, b, q, W, j0, start);
             ++nev;
         }
         if (w.cmask) apply_last(w, nce, fr_start, dinact);
@@ -924,6 +926,8 @@ struct Dec {
                 e[3] = A;
                 e[4] = W;
             }
+            if (a->ev_xhat && e_ix < a->ev_cap)  // the block is <= 32 aligned rows
+                atomicOr(&a->ev_xhat[((long long)frame_ * a->ev_cap + e_ix) * NW + (A >> 5)], xb << (A & 31));
         }
         prot |= __reduce_or_sync(kFull, myprot);
         nev += __popc(cmask);

@@ -123,6 +123,7 @@ struct pbp_ctx {
     DevBuf<double> llr64;
     DevBuf<uint32_t> ubits;
     DevBuf<int> iters, nev, events;
+    DevBuf<uint32_t> evx;  // trace: each event's x_hat bits
     DevBuf<long long> pe;
     DevBuf<uint8_t> stop;
     int last_launches = 0;
@@ -189,6 +190,7 @@ struct DecodeReq {
     int* nev = nullptr;
     int* events = nullptr;
     int ev_cap = 0;
+    uint32_t* ev_xhat = nullptr;
     const uint32_t* truth = nullptr;
     unsigned long long* counters = nullptr;
     bool force_generic = false;
@@ -296,6 +298,7 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
     a.nev = r.nev;
     a.events = r.events;
     a.ev_cap = r.ev_cap;
+    a.ev_xhat = r.ev_xhat;
     a.truth_u = r.truth;
     a.counters = r.counters;
     a.list_len = s.ctl.p + 2;
@@ -378,6 +381,7 @@ int run_generic_list(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream
     a.nev = r.nev;
     a.events = r.events;
     a.ev_cap = r.ev_cap;
+    a.ev_xhat = r.ev_xhat;
     a.truth_u = r.truth;
     a.counters = r.counters;
     a.list = r.list;
@@ -502,6 +506,7 @@ int pbp_ctx_destroy(pbp_ctx* ctx) {
     ctx->iters.release();
     ctx->nev.release();
     ctx->events.release();
+    ctx->evx.release();
     ctx->pe.release();
     ctx->stop.release();
     cudaStreamDestroy(ctx->stream);
@@ -756,7 +761,8 @@ namespace {
 // decode_csfg(..., events) for one frame; fp32 (llrs) or fp64 (llrs64)
 int decode_trace_impl(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs, const double* llrs64,
                       double alpha, int32_t max_iter, uint8_t* u_hat, int32_t* iterations, int64_t* pe,
-                      int32_t* stop, int32_t* n_events, int32_t* events, int32_t events_cap) {
+                      int32_t* stop, int32_t* n_events, int32_t* events, int32_t events_cap,
+                      uint32_t* events_xhat) {
     if (!ctx) return fail(PBP_EINVAL, "null context");
     PBP_CUDA(cudaSetDevice(ctx->device));
     int rc = upload_code(ctx, code);
@@ -769,6 +775,11 @@ int decode_trace_impl(pbp_ctx* ctx, const pbp_code* code, int decoder, const flo
         return rc;
     cudaStream_t st = ctx->stream;
     DecodeReq r;
+    if (events_xhat) {
+        if ((rc = ctx->evx.ensure((size_t)cap * nw))) return rc;
+        PBP_CUDA(cudaMemsetAsync(ctx->evx.p, 0, (size_t)cap * nw * 4, st));
+        r.ev_xhat = ctx->evx.p;
+    }
     if (llrs64) {
         if ((rc = ctx->llr64.ensure(n))) return rc;
         PBP_CUDA(cudaMemcpyAsync(ctx->llr64.p, llrs64, (size_t)n * 8, cudaMemcpyHostToDevice, st));
@@ -802,6 +813,8 @@ int decode_trace_impl(pbp_ctx* ctx, const pbp_code* code, int decoder, const flo
     PBP_CUDA(cudaMemcpyAsync(&ne, ctx->nev.p, 4, cudaMemcpyDeviceToHost, st));
     std::vector<int> ev((size_t)cap * 5);
     PBP_CUDA(cudaMemcpyAsync(ev.data(), ctx->events.p, ev.size() * 4, cudaMemcpyDeviceToHost, st));
+    if (events_xhat && events_cap > 0)
+        PBP_CUDA(cudaMemcpyAsync(events_xhat, ctx->evx.p, (size_t)events_cap * nw * 4, cudaMemcpyDeviceToHost, st));
     PBP_CUDA(cudaStreamSynchronize(st));
     sp8 = s8;
     if (u_hat)
@@ -822,7 +835,14 @@ int pbp_decode_trace(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
                      int32_t max_iter, uint8_t* u_hat, int32_t* iterations, int64_t* pe, int32_t* stop,
                      int32_t* n_events, int32_t* events, int32_t events_cap) {
     return decode_trace_impl(ctx, code, decoder, llrs, nullptr, alpha, max_iter, u_hat, iterations, pe, stop,
-                             n_events, events, events_cap);
+                             n_events, events, events_cap, nullptr);
+}
+
+int pbp_decode_trace_x(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs, float alpha,
+                       int32_t max_iter, uint8_t* u_hat, int32_t* iterations, int64_t* pe, int32_t* stop,
+                       int32_t* n_events, int32_t* events, int32_t events_cap, uint32_t* events_xhat) {
+    return decode_trace_impl(ctx, code, decoder, llrs, nullptr, alpha, max_iter, u_hat, iterations, pe, stop,
+                             n_events, events, events_cap, events_xhat);
 }
 
 int pbp_decode_trace_f64(pbp_ctx* ctx, const pbp_code* code, int decoder, const double* llrs, double alpha,
@@ -830,7 +850,15 @@ int pbp_decode_trace_f64(pbp_ctx* ctx, const pbp_code* code, int decoder, const 
                          int32_t* n_events, int32_t* events, int32_t events_cap) {
     if (!llrs) return fail(PBP_EINVAL, "null llrs");
     return decode_trace_impl(ctx, code, decoder, nullptr, llrs, alpha, max_iter, u_hat, iterations, pe, stop,
-                             n_events, events, events_cap);
+                             n_events, events, events_cap, nullptr);
+}
+
+int pbp_decode_trace_f64_x(pbp_ctx* ctx, const pbp_code* code, int decoder, const double* llrs, double alpha,
+                           int32_t max_iter, uint8_t* u_hat, int32_t* iterations, int64_t* pe, int32_t* stop,
+                           int32_t* n_events, int32_t* events, int32_t events_cap, uint32_t* events_xhat) {
+    if (!llrs) return fail(PBP_EINVAL, "null llrs");
+    return decode_trace_impl(ctx, code, decoder, nullptr, llrs, alpha, max_iter, u_hat, iterations, pe, stop,
+                             n_events, events, events_cap, events_xhat);
 }
 
 int pbp_decode_batch_f64_device(pbp_ctx* ctx, const pbp_code* code, int decoder, const double* llrs_dev,

@@ -39,6 +39,9 @@ struct DecodeArgs {
     int* nev;
     int* events;  // frames x ev_cap x 5 (nullable)
     int ev_cap;
+    // frames x ev_cap x ceil(n/32) words, zeroed (nullable): each event's x_hat,
+    // the block's hard decisions at its rows (FreezeEvent::x_hat)
+    uint32_t* ev_xhat;
     // counters mode (nullable)
     const uint32_t* truth_u;          // frames x ceil(n/32)
     unsigned long long* counters;     // kNumCounters

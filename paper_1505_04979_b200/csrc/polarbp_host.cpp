@@ -338,22 +338,29 @@ DecodeOutcome one_frame(const PolarCode& code, int kind, std::span<const T> llrs
     out.u_hat.assign(code.n, 0);
     int32_t it = 0, stop = 0, nev = 0;
     int64_t pe = 0;
-    const int cap = 4096;
+    const int cap = 4096, nw = (code.n + 31) / 32;
     std::vector<int32_t> ev(events ? static_cast<size_t>(cap) * 5 : 5);
+    std::vector<uint32_t> xw(events ? static_cast<size_t>(cap) * nw : 0);  // each event's x_hat
+    uint32_t* xp = events ? xw.data() : nullptr;
     if constexpr (sizeof(T) == 8)
-        raise(pbp_decode_trace_f64(ctx(), &v, kind, llrs.data(), alpha, max_iter, out.u_hat.data(), &it, &pe, &stop,
-                                   &nev, ev.data(), events ? cap : 1));
+        raise(pbp_decode_trace_f64_x(ctx(), &v, kind, llrs.data(), alpha, max_iter, out.u_hat.data(), &it, &pe,
+                                     &stop, &nev, ev.data(), events ? cap : 1, xp));
     else
-        raise(pbp_decode_trace(ctx(), &v, kind, llrs.data(), static_cast<float>(alpha), max_iter, out.u_hat.data(),
-                               &it, &pe, &stop, &nev, ev.data(), events ? cap : 1));
+        raise(pbp_decode_trace_x(ctx(), &v, kind, llrs.data(), static_cast<float>(alpha), max_iter,
+                                 out.u_hat.data(), &it, &pe, &stop, &nev, ev.data(), events ? cap : 1, xp));
     out.info_bits = extract_info_bits(code, out.u_hat);
     out.iterations_used = it;
     out.pe_activations = pe;
     out.stop_reason = static_cast<StopReason>(stop);
     if (events) {
         events->clear();
-        for (int i = 0; i < std::min(nev, cap); ++i)
-            events->push_back({ev[5 * i], ev[5 * i + 1], ev[5 * i + 2], ev[5 * i + 3], ev[5 * i + 4], {}});
+        for (int i = 0; i < std::min(nev, cap); ++i) {
+            FreezeEvent fe{ev[5 * i], ev[5 * i + 1], ev[5 * i + 2], ev[5 * i + 3], ev[5 * i + 4], {}};
+            const uint32_t* w = xw.data() + static_cast<size_t>(i) * nw;
+            fe.x_hat.resize(fe.size);
+            for (int r = 0; r < fe.size; ++r) fe.x_hat[r] = (w[(fe.start + r) >> 5] >> ((fe.start + r) & 31)) & 1u;
+            events->push_back(std::move(fe));
+        }
     }
     return out;
 }

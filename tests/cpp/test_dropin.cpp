@@ -317,9 +317,9 @@ static void gpu_cases() {
     // acceptance.cpp:209-272, 275-300 (criterion 6): 10^4 random small codes, lengths,
     // rates, design points, iteration caps and Eb/N0 - frozen-bit safety of csfg and
     // G-stop, prefix-only frontier growth with increasing (iteration, stage) stamps,
-    // per-iteration activation counts that never increase, and the replayed total equal
-    // to the reported PE count (the decided-prefix part needs FreezeEvent::x_hat, which
-    // the GPU trace does not carry)
+    // per-iteration activation counts that never increase, the replayed total equal to
+    // the reported PE count, and the decided prefix of u_hat equal to the events'
+    // polar_transform(x_hat) applied in order (each committed block frozen-consistent)
     {
         std::mt19937_64 gen(9006);
         std::uniform_real_distribution<double> unif(0.0, 1.0);
@@ -347,7 +347,16 @@ static void gpu_cases() {
             long long f = 0;
             int pi = 0, ps = 0;
             bool ok = true;
+            Bits decided(n, 0);
             for (const FreezeEvent& ev : evs) {
+                ok = ok && static_cast<int>(ev.x_hat.size()) == ev.size;
+                if (static_cast<int>(ev.x_hat.size()) == ev.size) {
+                    const Bits ub = polar_transform(ev.x_hat);
+                    for (int i = 0; i < ev.size; ++i) {
+                        ok = ok && !(code.frozen[ev.start + i] && ub[i]);
+                        decided[ev.start + i] = ub[i];
+                    }
+                }
                 const int size = n >> (ev.stage + 1);
                 ok = ok && ev.size == size && size > 0 && ev.start % size == 0 && ev.block == ev.start / size &&
                      ev.start <= f && ev.start + ev.size > f &&
@@ -357,6 +366,7 @@ static void gpu_cases() {
                 f = ev.start + ev.size;
             }
             ok = ok && (oc.stop_reason == StopReason::csfg_complete) == (f == n);
+            for (int r = 0; r < f; ++r) ok = ok && oc.u_hat[r] == decided[r];
             frontier_bad += !ok;
             FreezeState fz(n);
             long long total = 0, prev = -1;

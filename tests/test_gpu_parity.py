@@ -412,3 +412,42 @@ def test_cta_kernel_random_frozen_sets(ctx, n, kind, rate):
     assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"])
     for f in ("iterations", "pe", "stop", "n_events"):
         assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), f
+
+
+@pytest.mark.parametrize("n", [64, 256, 1024, 4096])
+def test_event_xhat_consistent(ctx, n):
+    """FreezeEvent.x_hat from every kernel (generic, warp-resident, CTA) and both
+    precisions: the fast and the generic kernel report the same blocks and bits, each
+    block's polar_transform(x_hat) is 0 at its frozen rows, and replaying the events'
+    decisions in order gives u_hat's decided prefix (acceptance.cpp:209-245)."""
+    fz = O.construct(n, n // 2, Z0)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    _, llr64 = O.trials(11, 0, 6, fz, 3.0 if n >= 1024 else 2.5, lib=O.C)
+    seen = 0
+    for i in range(llr64.shape[0]):
+        for prec in ("f32", "f64"):
+            runs = []
+            for generic in ((False, True) if prec == "f32" else (False,)):
+                ctx.force_generic(generic)
+                try:
+                    ev = []
+                    out = P.decode_csfg(code, llr64[i], 0.9375, 40, events=ev, ctx=ctx, precision=prec)
+                finally:
+                    ctx.force_generic(False)
+                runs.append((out, ev))
+            out, ev = runs[0]
+            if len(runs) == 2:
+                assert [(e.iteration, e.stage, e.start, e.size) for e in ev] == \
+                       [(e.iteration, e.stage, e.start, e.size) for e in runs[1][1]]
+                assert all(np.array_equal(a.x_hat, b.x_hat) for a, b in zip(ev, runs[1][1]))
+            decided = np.zeros(n, np.uint8)
+            f = 0
+            for e in ev:
+                assert e.x_hat is not None and len(e.x_hat) == e.size
+                ub = P.polar_transform(e.x_hat)
+                assert not np.any(ub & fz[e.start:e.start + e.size])
+                decided[e.start:e.start + e.size] = ub
+                f = e.start + e.size
+            assert np.array_equal(out.u_hat[:f], decided[:f])
+            seen += len(ev)
+    assert seen > 0
