@@ -181,7 +181,9 @@ extern "C" int pbp_prof_read(unsigned long long* out, int reset) {
 #define PBP_T1(v, k)
 #endif
 
-template <int M, int KIND>
+// XH: also record each freeze event's x_hat (trace calls; a separate
+// instantiation keeps the decode kernel's code unchanged)
+template <int M, int KIND, bool XH = false>
 struct Dec {
 #ifdef PBP_PROF_SECTIONS
     unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -823,7 +825,7 @@ struct Dec {
                 e[3] = start;
                 e[4] = sz;
             }
-            if (a->ev_xhat && nev < a->ev_cap)  // FreezeEvent::x_hat (trace calls only)
+            if (XH && a->ev_xhat && nev < a->ev_cap)  // FreezeEvent::x_hat (trace calls only)
                 scatter(a->ev_xhat + ((long long)frame_ * a->ev_cap + nev) * NW, xbits, in_block, b, q, W, j0, start);
             ++nev;
         }
@@ -926,7 +928,7 @@ struct Dec {
                 e[3] = A;
                 e[4] = W;
             }
-            if (a->ev_xhat && e_ix < a->ev_cap)  // the block is <= 32 aligned rows
+            if (XH && a->ev_xhat && e_ix < a->ev_cap)  // the block is <= 32 aligned rows
                 atomicOr(&a->ev_xhat[((long long)frame_ * a->ev_cap + e_ix) * NW + (A >> 5)], xb << (A & 31));
         }
         prot |= __reduce_or_sync(kFull, myprot);
@@ -1294,11 +1296,11 @@ struct Dec {
 template <int M>
 constexpr int kMinWarps = M >= 10 ? 1 : (M == 9 ? 12 : 20);
 
-template <int M, int KIND>
+template <int M, int KIND, bool XH = false>
 __global__ void __launch_bounds__(32, kMinWarps<M>) bp_warp_kernel(DecodeArgs a) {
     extern __shared__ __align__(16) unsigned char wsm[];
-    Dec<M, KIND> dec;
-    dec.run(a, reinterpret_cast<typename Dec<M, KIND>::Smem*>(wsm), threadIdx.x & 31);
+    Dec<M, KIND, XH> dec;
+    dec.run(a, reinterpret_cast<typename Dec<M, KIND, XH>::Smem*>(wsm), threadIdx.x & 31);
 }
 
 }  // namespace wk
@@ -1316,14 +1318,22 @@ size_t warp_smem_bytes(int m, int kind) {
     return 0;
 }
 
-template <int M, int KIND>
-static cudaError_t launch_w(const DecodeArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = sizeof(typename wk::Dec<M, KIND>::Smem);
-    cudaError_t e = cudaFuncSetAttribute(wk::bp_warp_kernel<M, KIND>,
+template <int M, int KIND, bool XH>
+static cudaError_t launch_wx(const DecodeArgs& a, int grid, cudaStream_t st) {
+    const size_t smem = sizeof(typename wk::Dec<M, KIND, XH>::Smem);
+    cudaError_t e = cudaFuncSetAttribute(wk::bp_warp_kernel<M, KIND, XH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    wk::bp_warp_kernel<M, KIND><<<grid, 32, smem, st>>>(a);
+    wk::bp_warp_kernel<M, KIND, XH><<<grid, 32, smem, st>>>(a);
     return cudaGetLastError();
+}
+
+template <int M, int KIND>
+static cudaError_t launch_w(const DecodeArgs& a, int grid, cudaStream_t st) {
+    if constexpr (KIND == 2) {
+        if (a.ev_xhat) return launch_wx<M, KIND, true>(a, grid, st);  // trace with x_hat
+    }
+    return launch_wx<M, KIND, false>(a, grid, st);
 }
 
 template <int M>
