@@ -142,7 +142,9 @@ struct Smem {
     long long frame;
 };
 
-template <int M, int KIND>
+// XH: also record each freeze event's x_hat (trace calls; a separate
+// instantiation keeps the decode kernel's code unchanged)
+template <int M, int KIND, bool XH = false>
 struct Dec {
     using PL = Plan<M>;
     using C = Cfg<M>;
@@ -494,7 +496,7 @@ struct Dec {
                 const uint32_t bit = 1u << (r & 31);
                 if ((u >> j) & 1u) atomicOr(&sm->dec[r >> 5], bit);
                 else atomicAnd(&sm->dec[r >> 5], ~bit);
-                if (a->ev_xhat && nev < a->ev_cap && ((x >> j) & 1u))
+                if (XH && a->ev_xhat && nev < a->ev_cap && ((x >> j) & 1u))
                     atomicOr(&a->ev_xhat[((long long)sm->frame * a->ev_cap + nev) * NW + (r >> 5)], bit);
             }
         }
@@ -695,21 +697,29 @@ struct Dec {
     }
 };
 
-template <int M, int KIND>
+template <int M, int KIND, bool XH = false>
 __global__ void __launch_bounds__(Plan<M>::T, Cfg<M>::MINB) bp_cta_kernel(const __grid_constant__ DecodeArgs a) {
     extern __shared__ __align__(16) unsigned char csm[];
-    Dec<M, KIND> dec;
+    Dec<M, KIND, XH> dec;
     dec.run(a, reinterpret_cast<Smem<M>*>(csm));
+}
+
+template <int M, int KIND, bool XH>
+static cudaError_t launch_tx(const DecodeArgs& a, int grid, cudaStream_t st) {
+    const size_t smem = sizeof(Smem<M>);
+    cudaError_t e = cudaFuncSetAttribute(bp_cta_kernel<M, KIND, XH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    bp_cta_kernel<M, KIND, XH><<<grid, Plan<M>::T, smem, st>>>(a);
+    return cudaGetLastError();
 }
 
 template <int M, int KIND>
 static cudaError_t launch_t(const DecodeArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = sizeof(Smem<M>);
-    cudaError_t e = cudaFuncSetAttribute(bp_cta_kernel<M, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    bp_cta_kernel<M, KIND><<<grid, Plan<M>::T, smem, st>>>(a);
-    return cudaGetLastError();
+    if constexpr (KIND == 2) {
+        if (a.ev_xhat) return launch_tx<M, KIND, true>(a, grid, st);  // trace with x_hat
+    }
+    return launch_tx<M, KIND, false>(a, grid, st);
 }
 
 template <int M>
