@@ -50,10 +50,10 @@ enum : int { kReg = 0, kSmem = 1, kGlob = 2, kBits = 3 };
 template <int M>
 struct Cfg;
 template <>
-struct Cfg<11> {  // 256 threads x 8 rows, 3 CTAs per SM (csfg +23 % over 512 x 4 at 2 per SM)
-    static constexpr int LOGT = 8, K = 3, MINB = 3;
+struct Cfg<11> {  // 128 threads x 16 rows, 3 CTAs per SM: four levels in registers, the rest in shared memory
+    static constexpr int LOGT = 7, K = 4, MINB = 3;
     static constexpr bool r0reg = false, rx2 = false;
-    static constexpr int where(int s) { return s == 11 ? kBits : (s == 1 || s == 2 || s == 4) ? kReg : kSmem; }
+    static constexpr int where(int s) { return s == 11 ? kBits : (s <= 3 || s == 5) ? kReg : kSmem; }
 };
 template <>
 struct Cfg<12> {  // 256 x 16, two frames per SM: four levels in registers, five in shared memory, two in L2
