@@ -377,11 +377,11 @@ long long generic_scratch_elems(int n, int m) {
 template <int BLOCK, typename T, bool SM>
 static cudaError_t launch_t(const DecodeArgs& a, int grid, cudaStream_t stream) {
     const size_t smem = SM ? smem_state_bytes(a.n, a.m, sizeof(T)) : generic_bits_bytes(a.n);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(bp_generic_kernel<BLOCK, T, SM>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
+    // always opt in: the kernel's static shared variables come on top of smem
+    // (n = 32768 needs exactly 48 KB dynamic)
+    cudaError_t e = cudaFuncSetAttribute(bp_generic_kernel<BLOCK, T, SM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     bp_generic_kernel<BLOCK, T, SM><<<grid, BLOCK, smem, stream>>>(a);
     return cudaGetLastError();
 }

@@ -134,8 +134,9 @@ namespace {
 
 int check_code(const pbp_code* code) {
     if (!code || !code->frozen) return fail(PBP_EINVAL, "pbp_code: null code or frozen mask");
-    if (!is_pow2(code->n) || code->n > (1 << 24))
-        return fail(PBP_EINVAL, "pbp_code: n must be a power of two <= 2^24");
+    // the generic decoder keeps a frame's bit state (1.5 n bytes) in shared memory
+    if (!is_pow2(code->n) || code->n > (1 << 17))
+        return fail(PBP_EINVAL, "pbp_code: n must be a power of two <= 131072");
     if (code->m != log2i(code->n)) return fail(PBP_EINVAL, "pbp_code: m != log2(n)");
     int frozen = 0;
     for (int i = 0; i < code->n; ++i) frozen += code->frozen[i] ? 1 : 0;

@@ -451,3 +451,29 @@ def test_event_xhat_consistent(ctx, n):
             assert np.array_equal(out.u_hat[:f], decided[:f])
             seen += len(ev)
     assert seen > 0
+
+
+@pytest.mark.parametrize("n", [32768, 65536])
+def test_generic_kernel_beyond_cta_sizes(ctx, n):
+    """n > 16384 decodes on the generic kernel (global-memory messages): parity with the
+    oracle for all three decoders."""
+    assert P.lib.pbp_kernel_path(n) == 0
+    fz = O.construct(n, n // 2, Z0)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    _, llr64 = O.trials(13, 0, 2, fz, 3.0, lib=O.C)
+    llr = llr64.astype(np.float32)
+    for kind in ("baseline", "gmatrix", "csfg"):
+        exp = O.decode_batch(kind, fz, llr, 0.9375, 12, prec=32)
+        got = P.decode_batch(code, kind, llr, 0.9375, 12, ctx=ctx)
+        assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"]), kind
+        for f in ("iterations", "pe", "stop", "n_events"):
+            assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), (kind, f)
+
+
+def test_code_length_limit(ctx):
+    """n above 131072 is refused with a message (the generic kernel's bit state lives in
+    shared memory), not a failed launch."""
+    n = 1 << 18
+    code = P.PolarCode.from_frozen_mask(n, np.r_[np.ones(n // 2, np.uint8), np.zeros(n // 2, np.uint8)])
+    with pytest.raises((ValueError, P._abi.PbpError), match="131072"):
+        P.decode_batch(code, "csfg", np.zeros((1, n), np.float32), 0.9375, 2, ctx=ctx)
