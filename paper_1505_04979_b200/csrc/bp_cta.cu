@@ -603,6 +603,8 @@ struct Dec {
                 for (int j = 0; j < P; ++j) Lr[l][j] = 0.f;
             lm_nz = fz<Q - 1>();
             lm_neg = 0u;
+#pragma unroll
+            for (int j = 0; j < P; ++j) R[j] = 0.f;  // R(m) = 0 until the first sweep (max_iter = 0)
             for (int i = tid; i < PL::NSM * PL::NX; i += kT) (&sm->Ls[0][0])[i] = 0.f;
             for (int i = tid; i < PL::NGL * N; i += kT) Lg[i] = 0.f;
             for (int r = tid; r < N; r += kT) sm->fst[r] = kNotFrozen;

@@ -29,6 +29,7 @@ def _oracle_batch(kind, fz, llr64, max_iter):
     (256, "csfg", 2.5, 128, 40, 5),
     (128, "csfg", 1.0, 64, 25, 7),
     (4096, "csfg", 2.5, 8, 60, 4),
+    (16384, "csfg", 2.5, 2, 40, 5),
 ])
 def test_f64_batch_matches_ref64(ctx, n, kind, ebn0, frames, max_iter, seed):
     fz = O.construct(n, n // 2, Z0)

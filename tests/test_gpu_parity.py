@@ -477,3 +477,18 @@ def test_code_length_limit(ctx):
     code = P.PolarCode.from_frozen_mask(n, np.r_[np.ones(n // 2, np.uint8), np.zeros(n // 2, np.uint8)])
     with pytest.raises((ValueError, P._abi.PbpError), match="131072"):
         P.decode_batch(code, "csfg", np.zeros((1, n), np.float32), 0.9375, 2, ctx=ctx)
+
+
+@pytest.mark.parametrize("n", [2048, 4096, 8192, 16384])
+def test_cta_kernel_iteration_caps_and_alpha(ctx, n):
+    """The CTA-per-frame kernel at max_iter 0/1/2/7 and other alphas."""
+    fz = O.construct(n, n // 2, Z0)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    llr = np.random.default_rng(n).normal(2.0, 1.5, size=(3, n)).astype(np.float32)
+    for kind in ("baseline", "gmatrix", "csfg"):
+        for alpha, mi in ((0.9375, 0), (0.9375, 1), (0.9375, 2), (0.5, 7), (1.0, 7)):
+            exp = O.decode_batch(kind, fz, llr, alpha, mi, prec=32)
+            got = P.decode_batch(code, kind, llr, alpha, mi, ctx=ctx)
+            assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"]), (kind, alpha, mi)
+            for f in ("iterations", "pe", "stop", "n_events"):
+                assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), (kind, alpha, mi, f)
