@@ -209,8 +209,11 @@ def test_channel_generation_matches_reference_stream(ctx, n, seed, ebn0):
     assert err.max() <= 8.0
 
 
-def test_simulate_point_counters_match_oracle(ctx):
-    n, seed, ebn0, frames = 1024, 2, 2.5, 384
+@pytest.mark.parametrize("n,frames", [(1024, 384), (256, 512), (2048, 64), (4096, 48), (16384, 6)])
+def test_simulate_point_counters_match_oracle(ctx, n, frames):
+    """run_point's counters (device generation, decode, bit errors against the sent
+    words) for every kernel against the oracle."""
+    seed, ebn0 = 2, 2.5
     fz = O.construct(n, n // 2, Z0)
     code = P.PolarCode.from_frozen_mask(n, fz)
     info, llr = O.trials(seed, 0, frames, fz, ebn0, lib=O.C)
