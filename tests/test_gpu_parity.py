@@ -495,3 +495,25 @@ def test_cta_kernel_iteration_caps_and_alpha(ctx, n):
             assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"]), (kind, alpha, mi)
             for f in ("iterations", "pe", "stop", "n_events"):
                 assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), (kind, alpha, mi, f)
+
+
+def test_chunked_batch_cta_kernel(ctx):
+    """The host pipeline at n = 4096 (CTA-per-frame kernel): several chunks, re-routed
+    frames in later chunks (frame_base of the batch-wide list), results equal to
+    one launch per part."""
+    n, frames = 4096, 9000
+    code = P.PolarCode.construct(n, n // 2, Z0)
+    llr, _, _ = P.generate(code, 4, 0, frames, 2.5, ctx=ctx)
+    big = [3, 4_500, 8_999]
+    llr[big, 11] = -1e30
+    whole = P.decode_batch(code, "csfg", llr, 0.9375, 20, ctx=ctx)
+    launches, rerouted = ctx.last_launch_info()
+    assert rerouted == len(big) and launches >= 2, (launches, rerouted)
+    for a, b in ((0, 4_000), (4_000, frames)):
+        part = P.decode_batch(code, "csfg", llr[a:b], 0.9375, 20, ctx=ctx)
+        for f in whole:
+            assert np.array_equal(whole[f][a:b], part[f]), (f, a)
+    exp = O.decode_batch("csfg", code.frozen, llr[big], 0.9375, 20, prec=32)
+    assert np.array_equal(P.unpack_bits(whole["u_hat_bits"][big], n), exp["u_hat"])
+    for f in ("iterations", "pe", "stop", "n_events"):
+        assert np.array_equal(whole[f][big].astype(np.int64), exp[f].astype(np.int64)), f
