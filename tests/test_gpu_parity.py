@@ -517,3 +517,25 @@ def test_chunked_batch_cta_kernel(ctx):
     assert np.array_equal(P.unpack_bits(whole["u_hat_bits"][big], n), exp["u_hat"])
     for f in ("iterations", "pe", "stop", "n_events"):
         assert np.array_equal(whole[f][big].astype(np.int64), exp[f].astype(np.int64)), f
+
+
+@pytest.mark.parametrize("n", [64, 1024, 4096])
+@pytest.mark.parametrize("k_of", ["all", "one", "last"])
+def test_degenerate_frozen_sets(ctx, n, k_of):
+    """k = n (every candidate check accepts), k = 1 with the free row first or last:
+    every decoder against the oracle."""
+    fz = np.ones(n, np.uint8)
+    if k_of == "all":
+        fz[:] = 0
+    elif k_of == "one":
+        fz[0] = 0
+    else:
+        fz[n - 1] = 0
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    llr = np.random.default_rng(n + len(k_of)).normal(1.5, 2.0, size=(5, n)).astype(np.float32)
+    for kind in ("baseline", "gmatrix", "csfg"):
+        exp = O.decode_batch(kind, fz, llr, 0.9375, 15, prec=32)
+        got = P.decode_batch(code, kind, llr, 0.9375, 15, ctx=ctx)
+        assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"]), kind
+        for f in ("iterations", "pe", "stop", "n_events"):
+            assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), (kind, f)
