@@ -539,3 +539,27 @@ def test_degenerate_frozen_sets(ctx, n, k_of):
         assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"]), kind
         for f in ("iterations", "pe", "stop", "n_events"):
             assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), (kind, f)
+
+
+@pytest.mark.parametrize("n", [2048, 4096, 16384])
+def test_cta_kernel_special_llr_values(ctx, n):
+    """Exact zeros, -0, denormals, values at the clamp-free bound (kept on the fast path)
+    and just above it (re-routed): the CTA-per-frame kernel against the oracle."""
+    fz = O.construct(n, n // 2, Z0)
+    code = P.PolarCode.from_frozen_mask(n, fz)
+    rng = np.random.default_rng(n)
+    llr = rng.normal(1.0, 2.0, size=(4, n)).astype(np.float32)
+    llr[0, ::7] = 0.0
+    llr[0, 3::7] = -0.0
+    llr[1, ::5] = np.float32(1e-42)
+    llr[1, 2::5] = -np.float32(1e-42)
+    llr[2, ::97] = np.float32(1e14)
+    llr[2, 1::97] = -np.float32(1e14)
+    llr[3, 17] = np.nextafter(np.float32(1e14), np.float32(np.inf))
+    for kind in ("gmatrix", "csfg"):
+        exp = O.decode_batch(kind, fz, llr, 0.9375, 25, prec=32)
+        got = P.decode_batch(code, kind, llr, 0.9375, 25, ctx=ctx)
+        assert ctx.last_launch_info()[1] == 1  # frame 3 only
+        assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"]), kind
+        for f in ("iterations", "pe", "stop", "n_events"):
+            assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), (kind, f)
