@@ -1002,8 +1002,9 @@ static int simulate_point_impl(pbp_ctx* ctx, const pbp_code* code, int decoder, 
     int rc = upload_code(ctx, code);
     if (rc) return rc;
     const int n = ctx->n, nw = (n + 31) / 32;
-    // chunk so the staging stays bounded (~256 MiB of LLRs)
-    const long long chunk = std::max<long long>(1, std::min<long long>(frames, (1ll << 26) / n));
+    // chunk so the staging stays bounded (512 MiB of fp32 LLRs: a config's 10^5-frame
+    // point at n = 1024 is one chunk, so one decode tail per point)
+    const long long chunk = std::max<long long>(1, std::min<long long>(frames, (1ll << 27) / n));
     // this call's slot: its generation staging and launch resources (an
     // asynchronous call may overlap other calls on other streams)
     DecodeSlot& sl = next_slot(ctx);

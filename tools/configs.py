@@ -62,9 +62,10 @@ def main():
             P._check(P.lib.pbp_decode_count_device(ctx.handle, C.byref(cs), kind, P._abi.f32p(llr.data_ptr()),
                                                    P._abi.u32p(u.data_ptr()), chunk, ALPHA, max_iter,
                                                    P._abi.i64p(wcnt.data_ptr()), C.c_void_p(stream.cuda_stream)))
-            P._check(P.lib.pbp_simulate_point_device(ctx.handle, C.byref(cs), kind, C.c_uint64(seed), 0, chunk, snrs[0],
-                                                     0, ALPHA, max_iter, P._abi.i64p(wcnt.data_ptr()),
-                                                     C.c_void_p(stream.cuda_stream)))
+            for _ in range(3):  # simulate_point rotates over the context's three launch slots
+                P._check(P.lib.pbp_simulate_point_device(ctx.handle, C.byref(cs), kind, C.c_uint64(seed), 0, chunk,
+                                                         snrs[0], 0, ALPHA, max_iter, P._abi.i64p(wcnt.data_ptr()),
+                                                         C.c_void_p(stream.cuda_stream)))
             stream.synchronize()
             for snr in snrs:
                 cnt = torch.zeros(10, dtype=torch.int64, device=dev)
