@@ -6,9 +6,10 @@ One JSON line per (config, n, Eb/N0): decode-only device time (frames generated 
 device beforehand, chunked so no chunk exceeds 2^28 LLRs), decoded info bits/s, PE
 activations/s and the fraction of the fp32 ALU roofline (9 ops per PE,
 148 x 128 x sm_max_mhz), average iterations, FER/BER, freeze events per frame, and the
-same point generated + decoded on the device (simulate_point_device) as gen_decode_bits_s.
+same point generated + decoded on the device (simulate_point_device) as gen_decode_bits_s,
+and e2e_bits_per_s: pbp_decode_batch from pinned host LLRs (wall clock, copies included).
 Config 4's multi-GPU sharding is bench.py's job; here it is the single-GPU rate per n."""
-import argparse, ctypes as C, json, math, os, sys
+import argparse, ctypes as C, json, math, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1505_04979_b200 as P
@@ -102,6 +103,23 @@ def main():
                 gms = g0.elapsed_time(g1)
                 stream.synchronize()
                 assert cnt2.tolist() == c, (c, cnt2.tolist())
+                # end to end through the host C ABI: pinned host LLRs in, per-frame results
+                # out (one staging chunk of generated frames; copies and decode pipelined
+                # by the library)
+                nf = min(chunk, frames)
+                host = torch.empty((nf, n), dtype=torch.float32, pin_memory=True)
+                host.copy_(llr[:nf])
+                outs = [torch.empty(x, dtype=t, pin_memory=True) for x, t in
+                        (((nf, nw), torch.int32), (nf, torch.int32), (nf, torch.int64), (nf, torch.uint8), (nf, torch.int32))]
+                fo = P._abi.PbpFrameOut(P._abi.u32p(outs[0].data_ptr()), P._abi.i32p(outs[1].data_ptr()),
+                                        P._abi.i64p(outs[2].data_ptr()), P._abi.u8p(outs[3].data_ptr()),
+                                        P._abi.i32p(outs[4].data_ptr()))
+                call = lambda: P._check(P.lib.pbp_decode_batch(ctx.handle, C.byref(cs), kind, P._abi.f32p(host.data_ptr()),
+                                                               nf, ALPHA, max_iter, C.byref(fo)))
+                call()
+                t0 = time.perf_counter()
+                call()
+                e2e_s = time.perf_counter() - t0
                 f = c[0]
                 pe_s = c[5] / (ms / 1e3)
                 print(json.dumps({
@@ -114,6 +132,7 @@ def main():
                     "stops": {"max_iter": c[7], "gmatrix": c[8], "complete": c[9]},
                     "gen_decode_ms": round(gms, 3),
                     "gen_decode_bits_per_s": round(f * (n // 2) / (gms / 1e3), 1),
+                    "e2e_bits_per_s": round(nf * (n // 2) / e2e_s, 1), "e2e_frames": nf,
                     "kernel_path": P.lib.pbp_kernel_path(n),
                 }), flush=True)
 
