@@ -39,11 +39,16 @@
 #include <type_traits>
 
 #include "pbp_common.cuh"
+#include "tmem.cuh"
 
 namespace pbp {
 namespace wk {
 
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef PBP_TMEM_G
+#define PBP_TMEM_G 32
+#endif
+constexpr int kTG = PBP_TMEM_G;  // TMEM columns per tcgen05.ld/st of a 32-value row
 __constant__ uint32_t c_jmask[5] = {0x55555555u, 0x33333333u, 0x0F0F0F0Fu, 0x00FF00FFu, 0x0000FFFFu};
 
 template <int M_>
@@ -97,16 +102,23 @@ struct Plan {
     // inside one lane; those checks read raw R rows of two lanes (see snap_rows)
     static constexpr int SL = (Q - 1) * K;  // first stage of the last pass
     static constexpr int NL = M - SL;       // stages in the last pass
+    // n = 1024: eight frames (warps) per CTA and per SM, each warp with 256
+    // TMEM columns of its lane quarter: R(0) [C_R0, +32), L(m) [C_LM, +32)
+    // and the csfg snapshots of R(1..5) [C_S + 32 s, +32), pass-0 layout
+    // (lane l, column j <-> row l + 32 j; L(m) in the last-pass layout)
+    static constexpr bool TM = (M == 10);
+    static constexpr int WARPS = TM ? 8 : 1;
+    static constexpr uint32_t C_R0 = 0, C_LM = 32, C_S = 64, C_LM0 = 224;  // C_LM0: L(m) at frame start
 };
 
 // LMB: L(m) as bit masks (csfg: frees 3.8 KB for an 8th warp per SM at n =
 // 1024); float4 slots otherwise (measured faster for the other decoders)
 template <int M, bool LMB = false>
-struct WarpSmem {
+struct alignas(16) WarpSmem {
     using PL = Plan<M>;
     float X[PL::Q - 1][PL::NX];            // pass boundaries: R(e) then L(e), padded rows
     float4 Ls[PL::NLS][PL::P / 4][32];     // lane-private L slots (last pass, n=1024)
-    float4 LM[LMB ? 1 : PL::P / 4][32];    // L(m), lane-private, last-pass layout (float slots)
+    float4 LM[(LMB || PL::TM) ? 1 : PL::P / 4][32];  // L(m), lane-private, last-pass layout (float slots; TMEM at n=1024)
     uint32_t lmz[32], lmn[32];             // L(m) in {0, +-CAP}: nonzero / negative bits per lane (LMB)
     uint32_t pm[PL::NLR + PL::NLS][32];    // per lane: rows whose L(s) is a frozen boundary
     uint32_t ss[PL::NLR][32];              // ... and their signs (register arrays)
@@ -116,7 +128,8 @@ struct WarpSmem {
     int tmp[32];
     unsigned long long cnt[16];            // per-warp counter accumulators
     uint32_t su[PL::SL][32];               // per stage < SL: block-transformed sign bits of R(s+1)
-    uint32_t sv[PL::SL][32];               // ... and violated groups, OR over a block's lanes
+                                           // (TM: per early commit k, u_hat of its block)
+    uint32_t sv[PL::TM ? 1 : PL::SL][32];  // ... and violated groups, OR over a block's lanes
     float rs[PL::NL][2][PL::P];            // per stage >= SL: R(s+1) of the two candidate lanes
     int cS[PL::M], cbi[PL::M];             // commits recorded by the walks of one iteration
     uint32_t frz[PL::NW];                  // frozen rows, row-order words
@@ -192,8 +205,10 @@ struct Dec {
     static constexpr int N = PL::N, P = PL::P, K = PL::K, Q = PL::Q, NW = PL::NW;
 
     using Smem = WarpSmem<M, KIND == 2>;
+    static constexpr bool TM = PL::TM;
     Smem* sm;
-    float4* r0g;  // this warp's channel LLRs in global scratch, lane-private pass-0 layout
+    float4* r0g;  // this warp's channel LLRs in global scratch, lane-private pass-0 layout (n < 1024)
+    uint32_t tb;  // this warp's TMEM columns (n = 1024)
     const DecodeArgs* a;
     int lane;
     float alpha;
@@ -255,7 +270,10 @@ struct Dec {
     template <int T>
     __device__ __forceinline__ void load_L(float (&Lt)[P]) {
         constexpr int q = PL::pass_of(T - 1);
-        if constexpr (T == M && KIND == 2) {
+        if constexpr (T == M && TM) {
+            tm::ld_row<kTG>(tb + PL::C_LM, Lt);
+            tm::wait_ld();
+        } else if constexpr (T == M && KIND == 2) {
             const uint32_t z = sm->lmz[lane], ng = sm->lmn[lane];
 #pragma unroll
             for (int j = 0; j < P; ++j) Lt[j] = ((z >> j) & 1u) ? (((ng >> j) & 1u) ? -kCap : kCap) : 0.f;
@@ -611,6 +629,102 @@ struct Dec {
         L1 = done_ ? -4 : frontier / P;
     }
 
+    // n = 1024 (TM): the reference's stage loop over the first pass
+    // (csfg_freeze.cpp:109-119) from the sweep's TMEM snapshots of R(1..5).
+    // At a fixed frontier F the candidate blocks of stages 0..4 (512 >> s
+    // rows: words j0_s = F/32 rounded down to 16 >> s, every lane) are
+    // checked together: their sign bits go to disjoint fields of one word per
+    // lane (16, 8, 4, 2 and 1 bits at offsets 0, 16, 24, 28, 30), so one
+    // in-word pass transforms the register bits of all five blocks, one
+    // 5-level butterfly across lanes their lane bits, and one OR-reduction of
+    // the frozen-row violations gives all five verdicts. The first accepting
+    // stage commits; the frontier moves and the later stages are evaluated
+    // again at the new frontier (rare: ~1 first-pass commit per frame at
+    // 3 dB). Commit side effects follow after the sweep (apply_commits).
+    __device__ __forceinline__ void walk0() {
+        static_assert(M == 10 && PL::SL == 5 && P == 32, "walk0: n = 1024 layout");
+        tm::wait_st();  // this sweep's snapshots
+        fr_start_ = frontier;
+        int nc = 0;
+        s_last_ = M - 1;
+        done_ = false;
+        uint32_t skip = 0u;  // stages already past (one decision per stage)
+        const uint32_t fz0 = FZ[0];
+#pragma unroll 1
+        while (true) {
+            const int jf = frontier >> 5;
+            const int j00 = jf & ~15, j01 = jf & ~7, j02 = jf & ~3, j03 = jf & ~1, j04 = jf;
+            // two load phases keep the peak at 16 extra registers (R(5) and
+            // the register L levels are live here)
+            float v0[16], v1[8], v2[4], v3[2], v4[1];
+            tm::ld16(tb + PL::C_S + j00, v0);
+            tm::wait_ld();
+            // sign bits, independent chains: bit i of a chain = element i
+            uint32_t c0 = 0u, c1 = 0u, c2 = 0u, c3 = 0u;
+#pragma unroll
+            for (int i = 7; i >= 0; --i) {
+                c0 = __funnelshift_l(__float_as_uint(v0[i]), c0, 1);
+                c1 = __funnelshift_l(__float_as_uint(v0[8 + i]), c1, 1);
+            }
+            tm::ld8(tb + PL::C_S + 32 + j01, v1);
+            tm::ld4(tb + PL::C_S + 64 + j02, v2);
+            tm::ld2(tb + PL::C_S + 96 + j03, v3);
+            tm::ld1(tb + PL::C_S + 128 + j04, v4);
+            tm::wait_ld();
+#pragma unroll
+            for (int i = 7; i >= 0; --i) c2 = __funnelshift_l(__float_as_uint(v1[i]), c2, 1);
+#pragma unroll
+            for (int i = 3; i >= 0; --i) c3 = __funnelshift_l(__float_as_uint(v2[i]), c3, 1);
+            c3 = __funnelshift_l(__float_as_uint(v3[1]), c3, 1);  // bits: v3[1] v2[3..0] -> shifted below
+            uint32_t u = __byte_perm(c0, c1, 0x7740) | (c2 << 16);  // c1 < 256: bytes 2, 3 zero
+            // c3 holds v2[3..0] at bits 4..1 and v3[1] at bit 0: rebuild fields 2..4
+            const uint32_t f2 = (c3 >> 1) & 0xFu;
+            const uint32_t f3 = ((__float_as_uint(v3[0]) >> 31) | ((c3 & 1u) << 1));
+            const uint32_t f4 = __float_as_uint(v4[0]) >> 31;
+            u |= (f2 << 24) | (f3 << 28) | (f4 << 30);
+            // polar transform inside every field (register bits), then across lanes
+            u ^= (u >> 1) & 0x55555555u;
+            u ^= (u >> 2) & 0x03333333u;
+            u ^= (u >> 4) & 0x000F0F0Fu;
+            u ^= (u >> 8) & 0x000000FFu;
+#pragma unroll
+            for (int gp = 0; gp < 5; ++gp) {
+                const uint32_t o = __shfl_xor_sync(kFull, u, 1 << gp);
+                if (!((lane >> gp) & 1)) u ^= o;
+            }
+            const uint32_t fzw = ((fz0 >> j00) & 0xFFFFu) | (((fz0 >> j01) & 0xFFu) << 16) |
+                                 (((fz0 >> j02) & 0xFu) << 24) | (((fz0 >> j03) & 3u) << 28) |
+                                 (((fz0 >> j04) & 1u) << 30);
+            const uint32_t V = __reduce_or_sync(kFull, u & fzw);
+            uint32_t acc = (uint32_t)((V & 0xFFFFu) == 0u) | ((uint32_t)(((V >> 16) & 0xFFu) == 0u) << 1) |
+                           ((uint32_t)(((V >> 24) & 0xFu) == 0u) << 2) | ((uint32_t)(((V >> 28) & 3u) == 0u) << 3) |
+                           ((uint32_t)(((V >> 30) & 1u) == 0u) << 4);
+            acc &= ~skip;
+            if (!acc) break;
+            const int st = __ffs(acc) - 1;
+            const int g = M - 1 - st;  // the block has 2^g rows
+            const int bi = frontier >> g;
+            if (lane == 0) {
+                sm->cS[nc] = st;
+                sm->cbi[nc] = bi;
+            }
+            // u_hat of the block in the pass-0 layout (bit j = row lane + 32 j), for apply_commits
+            const int W = 16 >> st, off = st == 0 ? 0 : (st == 1 ? 16 : (st == 2 ? 24 : (st == 3 ? 28 : 30)));
+            sm->su[nc][lane] = ((u >> off) & low_mask(W)) << (jf & ~(W - 1));
+            ++nc;
+            frontier = (bi + 1) << g;
+            if (frontier >= N) {
+                s_last_ = st;
+                done_ = true;
+                break;
+            }
+            skip = (2u << st) - 1u;
+            if (st == PL::SL - 1) break;
+        }
+        nce_ = nc;
+        L1 = done_ ? -4 : frontier / P;
+    }
+
     // last-pass stage S: lanes L1 and L1+1 keep R(S+1) (rows P*lane + j)
     template <int S>
     __device__ __forceinline__ void snap_rows() {
@@ -738,7 +852,7 @@ struct Dec {
             const uint32_t msk = in_block ? (wm << j0) : 0u;
             const int sz = 1 << g, start = bi << g;
             // u_hat of the block; x_hat = T(u_hat) (the transform is an involution)
-            const uint32_t uu = sm->su[S][lane];
+            const uint32_t uu = TM ? sm->su[k][lane] : sm->su[S][lane];
             uint32_t xx = uu;
 #pragma unroll 1
             for (int tp = 0; tp < g - b; ++tp) xx ^= (xx >> (1 << tp)) & c_jmask[tp];
@@ -885,13 +999,29 @@ struct Dec {
             const int T = Sr + 1;
             const int owner = r / P, j = r % P;  // last-pass layout: row = P*lane + j
             if (T == M) {  // one row per iteration: a plain read-modify-write of the owner's bits
-                sm->lmz[owner] |= 1u << j;
-                sm->lmn[owner] = (sm->lmn[owner] & ~(1u << j)) | (xbit << j);
+                if constexpr (!TM) {
+                    sm->lmz[owner] |= 1u << j;
+                    sm->lmn[owner] = (sm->lmn[owner] & ~(1u << j)) | (xbit << j);
+                }
             } else if ((SMEMM >> T) & 1u) {
                 float* base = reinterpret_cast<float*>(&sm->Ls[__popc(SMEMM & ((1u << T) - 1u))][0][0]);
                 base[((j >> 2) * 32 + owner) * 4 + (j & 3)] = xbit ? -kCap : kCap;
             }
             sm->fst[r] = (uint8_t)Sr;
+        }
+        if constexpr (TM) {
+            // L(m) of the stage m-1 block (one row) in TMEM: column j of lane owner
+            if ((cmask >> (NL - 1)) & 1u) {
+                const int r9 = __shfl_sync(kFull, w.Al, NL - 1);
+                const uint32_t xb = (w.x[NL - 1] >> (r9 - w.A5)) & 1u;
+                const int j = r9 % P;
+                float v;
+                tm::ld1(tb + PL::C_LM + j, &v);
+                tm::wait_ld();
+                if (lane == r9 / P) v = xb ? -kCap : kCap;
+                tm::st1(tb + PL::C_LM + j, v);
+                tm::wait_st();
+            }
         }
         // 2. decided_u (:87), protection masks, event log (:91-92): lane t
         uint32_t myprot = 0u;
@@ -975,13 +1105,18 @@ struct Dec {
         constexpr bool last_of_pass = (S == PL::last(q));
         if constexpr (S == 0) {
             if constexpr (KIND != 0) xq = 0u;
+            if constexpr (TM) {
+                tm::ld_row<kTG>(tb + PL::C_R0, R);
+                tm::wait_ld();
+            } else {
 #pragma unroll
-            for (int c = 0; c < P / 4; ++c) {
-                const float4 v = r0g[c * 32 + lane];
-                R[4 * c] = v.x;
-                R[4 * c + 1] = v.y;
-                R[4 * c + 2] = v.z;
-                R[4 * c + 3] = v.w;
+                for (int c = 0; c < P / 4; ++c) {
+                    const float4 v = r0g[c * 32 + lane];
+                    R[4 * c] = v.x;
+                    R[4 * c + 1] = v.y;
+                    R[4 * c + 2] = v.z;
+                    R[4 * c + 3] = v.w;
+                }
             }
         } else if constexpr (first_of_pass) {
             x_load<q>(sm->X[q - 1], R);
@@ -1004,7 +1139,10 @@ struct Dec {
         PBP_T1(tm, 0);
         if constexpr (KIND == 2) {
             PBP_T0(ts);
-            if constexpr (S < PL::SL) {
+            if constexpr (S < PL::SL && TM) {
+                tm::st_row<kTG>(tb + PL::C_S + 32u * S, R);  // R(S+1), pass-0 layout
+                if constexpr (S == PL::SL - 1) walk0();
+            } else if constexpr (S < PL::SL) {
                 snapshot<S>();
                 if constexpr (S == PL::SL - 1) walk_early();
             } else {
@@ -1085,12 +1223,20 @@ struct Dec {
 
     __device__ __forceinline__ void run(const DecodeArgs& args, Smem* s, int ln) {
         a = &args;
-        r0g = reinterpret_cast<float4*>(args.r0s) + (long long)blockIdx.x * (N / 4);
+        r0g = TM ? nullptr : reinterpret_cast<float4*>(args.r0s) + (long long)blockIdx.x * (N / 4);
         sm = s;
         lane = ln;
         alpha = args.alpha;
         fz_init<0>();
         if (lane < NW) sm->frz[lane] = a->frozen_bits[lane];
+        if constexpr (TM) {
+            // L(m) at frame start: +CAP at frozen rows (bp_core.cpp:53), last-pass layout
+            const uint32_t fl = FZ[Q - 1];
+#pragma unroll
+            for (int j = 0; j < P; ++j) R[j] = ((fl >> j) & 1u) ? kCap : 0.f;
+            tm::st_row<kTG>(tb + PL::C_LM0, R);
+            tm::wait_st();
+        }
         // stage 0 pushes x_hat bits of rows (lane + 32 j) in the order
         // j = j0, j0+1, j0+d, j0+d+1 for j0 = 0, 2, ... (d = P/2); the first push
         // lands in bit 31. xperm = bit position that holds row-order word `lane`.
@@ -1225,8 +1371,21 @@ struct Dec {
         }
         __syncwarp();
         // each lane keeps its own slots: it is the only reader (stage 0)
+        if constexpr (TM) {
 #pragma unroll
-        for (int c = 0; c < P / 4; ++c) r0g[c * 32 + lane] = reinterpret_cast<const float4*>(r0)[c * 32 + lane];
+            for (int c = 0; c < P / 4; ++c) {
+                const float4 t = reinterpret_cast<const float4*>(r0)[c * 32 + lane];
+                R[4 * c] = t.x;
+                R[4 * c + 1] = t.y;
+                R[4 * c + 2] = t.z;
+                R[4 * c + 3] = t.w;
+            }
+            tm::st_row<kTG>(tb + PL::C_R0, R);
+            tm::wait_st();
+        } else {
+#pragma unroll
+            for (int c = 0; c < P / 4; ++c) r0g[c * 32 + lane] = reinterpret_cast<const float4*>(r0)[c * 32 + lane];
+        }
         __syncwarp();  // X is overwritten next
         return !__any_sync(kFull, bad);
     }
@@ -1242,13 +1401,13 @@ struct Dec {
     }
 
     __device__ __forceinline__ void init_frame() {
+        init_smem();
 #pragma unroll
         for (int j = 0; j < P; ++j) R[j] = 0.f;  // R(m) = 0 until the first sweep (max_iter = 0)
 #pragma unroll
         for (int sl = 0; sl < PL::NLR; ++sl)
 #pragma unroll
             for (int j = 0; j < P; ++j) Lr[sl][j] = 0.f;
-        init_smem();
         frontier = 0;
         inact = 0;
         nev = 0;
@@ -1267,7 +1426,16 @@ struct Dec {
 #pragma unroll 1
             for (int i = lane; i < PL::NX; i += 32) sm->X[x][i] = 0.f;
         // L(m): +CAP at frozen rows (bp_core.cpp:53), last-pass layout
-        if constexpr (KIND == 2) {
+        if constexpr (TM) {
+            // copied from the warp's pristine L(m) columns (written once in
+            // run(): computing the 32 values here lets the compiler hoist them
+            // out of the frame loop, 32 registers live across the decode);
+            // R is the staging register set (init_frame zeroes it afterwards)
+            tm::ld_row<kTG>(tb + PL::C_LM0, R);
+            tm::wait_ld();
+            tm::st_row<kTG>(tb + PL::C_LM, R);
+            tm::wait_st();
+        } else if constexpr (KIND == 2) {
             sm->lmz[lane] = FZ[Q - 1];
             sm->lmn[lane] = 0u;
         } else {
@@ -1296,16 +1464,36 @@ struct Dec {
 template <int M>
 constexpr int kMinWarps = M >= 10 ? 1 : (M == 9 ? 12 : 20);
 
+// n = 1024: eight warps (frames) per CTA, one CTA per SM, so the CTA's TMEM
+// allocation (all 512 columns) gives each warp 256 columns of its lane quarter
 template <int M, int KIND, bool XH = false>
-__global__ void __launch_bounds__(32, kMinWarps<M>) bp_warp_kernel(DecodeArgs a) {
+__global__ void __launch_bounds__(32 * Plan<M>::WARPS, Plan<M>::TM ? 1 : kMinWarps<M>) bp_warp_kernel(DecodeArgs a) {
     extern __shared__ __align__(16) unsigned char wsm[];
-    Dec<M, KIND, XH> dec;
-    dec.run(a, reinterpret_cast<typename Dec<M, KIND, XH>::Smem*>(wsm), threadIdx.x & 31);
+    using D = Dec<M, KIND, XH>;
+    D dec;
+    if constexpr (Plan<M>::TM) {
+        __shared__ uint32_t tbase;
+        const int warp = threadIdx.x >> 5;
+        if (warp == 0) tm::alloc512(&tbase);
+        tm::fence_before();
+        __syncthreads();
+        tm::fence_after();
+        dec.tb = tm::warp_base(tbase, warp);
+        dec.run(a, reinterpret_cast<typename D::Smem*>(wsm) + warp, threadIdx.x & 31);
+        tm::fence_before();
+        __syncthreads();
+        tm::fence_after();
+        if (warp == 0) tm::dealloc512(tbase);
+    } else {
+        dec.run(a, reinterpret_cast<typename D::Smem*>(wsm), threadIdx.x & 31);
+    }
 }
 
 }  // namespace wk
 
 int warp_kernel_supported(int m) { return m >= 7 && m <= 10; }
+// warps (frames) per CTA of the warp kernel: eight at n = 1024 (TMEM), else one
+int warp_kernel_warps(int m) { return m == 10 ? wk::Plan<10>::WARPS : 1; }
 
 size_t warp_smem_bytes(int m, int kind) {
     const bool b = kind == 2;
@@ -1320,11 +1508,12 @@ size_t warp_smem_bytes(int m, int kind) {
 
 template <int M, int KIND, bool XH>
 static cudaError_t launch_wx(const DecodeArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = sizeof(typename wk::Dec<M, KIND, XH>::Smem);
+    constexpr int W = wk::Plan<M>::WARPS;
+    const size_t smem = W * sizeof(typename wk::Dec<M, KIND, XH>::Smem);
     cudaError_t e = cudaFuncSetAttribute(wk::bp_warp_kernel<M, KIND, XH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    wk::bp_warp_kernel<M, KIND, XH><<<grid, 32, smem, st>>>(a);
+    wk::bp_warp_kernel<M, KIND, XH><<<grid, 32 * W, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -1358,9 +1547,10 @@ cudaError_t launch_warp(const DecodeArgs& a, int grid, cudaStream_t st) {
 template <int M, int KIND>
 static int occ_w() {
     int nb = 0;
-    const size_t smem = sizeof(typename wk::Dec<M, KIND>::Smem);
+    constexpr int W = wk::Plan<M>::WARPS;
+    const size_t smem = W * sizeof(typename wk::Dec<M, KIND>::Smem);
     cudaFuncSetAttribute(wk::bp_warp_kernel<M, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wk::bp_warp_kernel<M, KIND>, 32, smem) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wk::bp_warp_kernel<M, KIND>, 32 * W, smem) != cudaSuccess)
         return 0;
     return nb;
 }

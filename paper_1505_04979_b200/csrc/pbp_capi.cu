@@ -24,6 +24,7 @@ bool generic_in_smem(int n, int m, bool f64);
 cudaError_t launch_warp(const DecodeArgs& a, int grid, cudaStream_t st);
 int warp_kernel_supported(int m);
 int warp_blocks_per_sm(int m, int kind);
+int warp_kernel_warps(int m);
 size_t warp_smem_bytes(int m, int kind);
 int cta_kernel_supported(int m);
 long long cta_scratch_floats(int m);
@@ -249,6 +250,7 @@ long long generic_grid(const pbp_ctx* ctx, long long frames, bool fast, int esz 
 // Size a slot's buffers for decodes of up to `frames` frames (before any
 // asynchronous work is queued: reallocation synchronises the device).
 int size_slot(pbp_ctx* ctx, DecodeSlot& s, int kind, long long frames) {
+    if (kind < 0 || kind > 2) return fail(PBP_EINVAL, "unknown decoder kind");  // indexes warp_occ
     int rc;
     if ((rc = s.ctl.ensure(4)) || (rc = s.list.ensure(std::max<long long>(frames, 1)))) return rc;
     size_t scratch = 0;
@@ -527,7 +529,8 @@ int pbp_kernel_info(int32_t n, int decoder, int32_t* smem_bytes, int32_t* warps_
     if (!is_pow2(n)) return fail(PBP_EINVAL, "pbp_kernel_info: n must be a power of two");
     const int m = log2i(n);
     if (smem_bytes) *smem_bytes = pbp::warp_kernel_supported(m) ? (int32_t)pbp::warp_smem_bytes(m, decoder) : 0;
-    if (warps_per_sm) *warps_per_sm = pbp::warp_kernel_supported(m) ? pbp::warp_blocks_per_sm(m, decoder) : 0;
+    if (warps_per_sm)
+        *warps_per_sm = pbp::warp_kernel_supported(m) ? pbp::warp_blocks_per_sm(m, decoder) * pbp::warp_kernel_warps(m) : 0;
     return PBP_OK;
 }
 
@@ -635,6 +638,7 @@ int pbp_decode_batch_device(pbp_ctx* ctx, const pbp_code* code, int decoder, con
 int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs,
                      int64_t frames, float alpha, int32_t max_iter, pbp_frame_out* out) {
     if (!ctx) return fail(PBP_EINVAL, "null context");
+    if (decoder < 0 || decoder > 2) return fail(PBP_EINVAL, "unknown decoder kind");
     if (frames < 0) return fail(PBP_EINVAL, "frames < 0");
     PBP_CUDA(cudaSetDevice(ctx->device));
     int rc = upload_code(ctx, code);

@@ -1,0 +1,114 @@
+// Tensor memory (TMEM) as per-warp scratch for the warp-resident decoder.
+//
+// The decoder has no dense contraction, so the tensor cores stay idle; their
+// 256 KB per SM of TMEM is used as a second on-chip store next to registers
+// and shared memory (tools/micro/tmem_rates.cu on this B200: ~480 B/clk/SM
+// tcgen05.ld and ~270 B/clk/SM tcgen05.st with 8 warps, against 128 B/clk of
+// shared memory; one instruction moves 32 columns per lane). A warp may only
+// touch the 32 TMEM lanes of its quarter (warp id % 4); each of the CTA's 8
+// warps owns 256 columns of its quarter. Addresses are warp-uniform.
+// TMEM is not C++-visible memory: the asm statements are volatile (kept in
+// program order among themselves) and carry no "memory" clobber, so the
+// compiler stays free to schedule shared/global accesses around them.
+#pragma once
+
+#include <cstdint>
+
+namespace pbp {
+namespace tm {
+
+// TMEM address of column `col` in the lane quarter of this warp
+__device__ __forceinline__ uint32_t warp_base(uint32_t base, int warp) {
+    return base + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2);
+}
+
+__device__ __forceinline__ void alloc512(uint32_t* smem_dst) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(smem_dst)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void dealloc512(uint32_t base) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base));
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;"); }
+__device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;"); }
+
+__device__ __forceinline__ void st32(uint32_t a, const float (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(a),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+        "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+        "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31]));
+}
+__device__ __forceinline__ void st8(uint32_t a, const float* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(a), "f"(v[0]),
+                 "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]));
+}
+__device__ __forceinline__ void st4(uint32_t a, const float* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3]));
+}
+// 32 columns as G-column pieces: each piece needs only G consecutive registers
+template <int G>
+__device__ __forceinline__ void st_row(uint32_t a, const float (&v)[32]) {
+#pragma unroll
+    for (int c = 0; c < 32; c += G) {
+        if constexpr (G == 8) st8(a + c, v + c);
+        else if constexpr (G == 4) st4(a + c, v + c);
+        else st32(a, v);
+    }
+}
+__device__ __forceinline__ void st1(uint32_t a, float v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(a), "f"(v));
+}
+
+__device__ __forceinline__ void ld32(uint32_t a, float (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]), "=f"(v[8]),
+          "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15]), "=f"(v[16]),
+          "=f"(v[17]), "=f"(v[18]), "=f"(v[19]), "=f"(v[20]), "=f"(v[21]), "=f"(v[22]), "=f"(v[23]), "=f"(v[24]),
+          "=f"(v[25]), "=f"(v[26]), "=f"(v[27]), "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
+        : "r"(a));
+}
+__device__ __forceinline__ void ld16(uint32_t a, float* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]), "=f"(v[8]),
+          "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+        : "r"(a));
+}
+__device__ __forceinline__ void ld8(uint32_t a, float* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "r"(a));
+}
+__device__ __forceinline__ void ld4(uint32_t a, float* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+                 : "r"(a));
+}
+template <int G>
+__device__ __forceinline__ void ld_row(uint32_t a, float (&v)[32]) {
+#pragma unroll
+    for (int c = 0; c < 32; c += G) {
+        if constexpr (G == 8) ld8(a + c, v + c);
+        else if constexpr (G == 4) ld4(a + c, v + c);
+        else ld32(a, v);
+    }
+}
+__device__ __forceinline__ void ld2(uint32_t a, float* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=f"(v[0]), "=f"(v[1]) : "r"(a));
+}
+__device__ __forceinline__ void ld1(uint32_t a, float* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=f"(v[0]) : "r"(a));
+}
+
+}  // namespace tm
+}  // namespace pbp
