@@ -811,18 +811,189 @@ struct Dec {
         done_ = done;
     }
 
+    // n = 1024 (TM): the reference's stage loop over the last pass
+    // (csfg_freeze.cpp:109-119). As walk_late, specialised: the window is the
+    // 32 rows from A5 = frontier rounded down to 16 (lanes L1, L1+1 stored
+    // them, rs[t] = R(6 + t)); lane t transforms stage 5 + t's window bits
+    // inside its blocks of 16 >> t rows and marks rejected blocks; the stage
+    // loop is a uniform scan.
+    struct LateTM {
+        int A5;
+        uint32_t x[PL::NL];  // window sign bits of R(6 + t) (uniform)
+        int At[PL::NL];      // block start of stage 5 + t at its check (uniform)
+        uint32_t u, xl;      // lane t: u_hat / x_hat bits of the window at stage 5 + t
+        int Al;              // lane t: At[t]
+        uint32_t cm;         // bit t: stage 5 + t committed
+    };
+    __device__ __forceinline__ void walk_tm(LateTM& w) {
+        static_assert(M == 10 && PL::SL == 5 && PL::NL == 5, "walk_tm: n = 1024 layout");
+        __syncwarp();  // rs rows
+        w.cm = 0u;
+        if (done_) return;
+        const int A5 = frontier & ~15;
+        w.A5 = A5;
+        const float* rsf = &sm->rs[0][0][0] + (A5 - P * L1);  // rs[t][c][j], t stride 2 P
+        uint32_t xl = 0u;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+            const uint32_t xt = __ballot_sync(kFull, __float_as_int(rsf[2 * P * t + lane]) < 0);
+            w.x[t] = xt;
+            xl = lane == t ? xt : xl;
+        }
+        const int w0 = A5 >> 5;
+        const uint32_t fw = (uint32_t)(((unsigned long long)sm->frz[w0] |
+                                        ((unsigned long long)(w0 + 1 < NW ? sm->frz[w0 + 1] : 0u) << 32)) >>
+                                       (A5 & 31));
+        const int g = 4 - lane;  // lane t < 5: log2 of its block size
+        uint32_t u = xl;
+#pragma unroll
+        for (int tp = 0; tp < 4; ++tp)
+            if (tp < g) u ^= (u >> (1 << tp)) & jmask(tp);
+        w.u = u;
+        w.xl = xl;
+        uint32_t viol = u & fw;
+#pragma unroll
+        for (int tp = 0; tp < 4; ++tp)
+            if (tp < g) viol |= viol >> (1 << tp);
+        int F = frontier, slast = s_last_, Al = 0;
+        uint32_t cm = 0u;
+        bool done = false;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+            const uint32_t vt = __shfl_sync(kFull, viol, t);
+            const int B = 16 >> t;
+            const int A = F & ~(B - 1);
+            w.At[t] = A;
+            Al = lane == t ? A : Al;
+            const bool acc = !done && !((vt >> (A - A5)) & 1u);
+            cm |= (uint32_t)acc << t;
+            F = acc ? A + B : F;
+            const bool fin = acc && F >= N;
+            slast = fin ? 5 + t : slast;
+            done = done || fin;
+        }
+        w.Al = Al;
+        w.cm = cm;
+        s_last_ = slast;
+        frontier = F;
+        done_ = done;
+    }
+
+    // apply_freeze (csfg_freeze.cpp:82-93) for the last-pass commits of one
+    // iteration (TM): lane i takes window row A5 + i (saturation of L(S+1),
+    // freeze_stage, decided_u by ballot), lane t takes stage 5 + t's commit
+    // (protection mask, event). The first commit of an iteration may re-cover
+    // rows decided before: their top rows already inactive at a stage s2 > S
+    // under their old freeze_stage are counted once (one packed warp sum).
+    __device__ __forceinline__ void apply_tm(const LateTM& w, int& dinact) {
+        const uint32_t cm = w.cm;
+        const int A5 = w.A5, r = A5 + lane;
+        int Sr = -1;
+        uint32_t xb = 0u;
+        int tr = 0;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+            if (((cm >> t) & 1u) && (unsigned)(r - w.At[t]) < (16u >> t)) {
+                Sr = 5 + t;
+                tr = t;
+                xb = (w.x[t] >> lane) & 1u;
+            }
+        }
+        const uint32_t ub = (__shfl_sync(kFull, w.u, tr) >> lane) & 1u;
+        const bool cov = Sr >= 0;
+        if (nce_ == 0) {
+            const bool rc = cov && r < fr_start_;
+            if (__any_sync(kFull, rc)) {
+                uint32_t pk = 0u;
+                if (rc) {
+                    const int fo = sm->fst[r];
+                    const int S0 = 5 + (__ffs(cm) - 1);
+                    const int lo = fo > S0 ? fo : S0;
+                    const uint32_t top = __brev(~(uint32_t)r) >> (32 - M);  // bit s2: top row at s2
+                    const uint32_t was = top & ~((2u << lo) - 1u);          // s2 in (lo, m)
+                    pk = ((was >> 6) & 1u) | (((was >> 7) & 1u) << 8) | (((was >> 8) & 1u) << 16) |
+                         (((was >> 9) & 1u) << 24);
+                }
+                const uint32_t c = __reduce_add_sync(kFull, pk);
+                if (lane >= 6 && lane < M) dinact -= (int)((c >> (8 * (lane - 6))) & 0xffu);
+            }
+        }
+        if (cov) {
+            const int owner = r >> 5, j = r & 31;
+            if (Sr < M - 1) {
+                float* base = reinterpret_cast<float*>(&sm->Ls[Sr - 5][0][0]);
+                base[((j >> 2) * 32 + owner) * 4 + (j & 3)] = xb ? -kCap : kCap;
+            }
+            sm->fst[r] = (uint8_t)Sr;
+        }
+        if ((cm >> 4) & 1u) {  // stage m-1: L(m) of one row, TMEM column j of lane owner
+            const int r9 = w.At[4];
+            const uint32_t x9 = (w.x[4] >> (r9 - A5)) & 1u;
+            const int j = r9 & 31;
+            float v;
+            tm::ld1(tb + PL::C_LM + j, &v);
+            tm::wait_ld();
+            if (lane == (r9 >> 5)) v = x9 ? -kCap : kCap;
+            tm::st1(tb + PL::C_LM + j, v);
+            tm::wait_st();
+        }
+        // decided_u over the window (two row-order words)
+        const uint32_t cvw = __ballot_sync(kFull, cov), uw = __ballot_sync(kFull, cov && ub);
+        if (lane < 2) {
+            const int wd = (A5 >> 5) + lane, sh = A5 & 31;
+            const uint32_t mk = lane == 0 ? cvw << sh : (sh ? cvw >> (32 - sh) : 0u);
+            const uint32_t vv = lane == 0 ? uw << sh : (sh ? uw >> (32 - sh) : 0u);
+            if (mk) sm->dec_u[wd] = (sm->dec_u[wd] & ~mk) | vv;
+        }
+        // inactive top rows: a stage-S block of B rows has B/2 top rows at every later stage
+        if (lane < M) dinact += (int)((__brev((cm << 5) & ((1u << lane) - 1u)) >> (32 - M)) >> 1);
+        if ((cm >> lane) & 1u) {
+            const int S = 5 + lane, B = 16 >> lane, A = w.Al;
+            const uint32_t wm = (1u << B) - 1u;
+            if (lane < 4) sm->pm[PL::NLR + lane][A >> 5] |= wm << (A & 31);  // L(S+1) in shared slot S - 5
+            const int e_ix = nev + __popc(cm & ((1u << lane) - 1u));
+            if (a->events && e_ix < a->ev_cap) {
+                int* e = a->events + ((long long)frame_ * a->ev_cap + e_ix) * 5;
+                e[0] = it;
+                e[1] = S;
+                e[2] = A >> (4 - lane);
+                e[3] = A;
+                e[4] = B;
+            }
+            if (XH && a->ev_xhat && e_ix < a->ev_cap)  // the block is <= 16 aligned rows
+                atomicOr(&a->ev_xhat[((long long)frame_ * a->ev_cap + e_ix) * NW + (A >> 5)],
+                         ((w.xl >> (A - A5)) & wm) << (A & 31));
+        }
+        prot |= (cm & 0xFu) << PL::NLR;
+        nev += __popc(cm);
+    }
+
     // after the sweep: late walk, side effects, stage_pass counts of stages
     // 0..s_last under the freeze state each ran with (a commit at stage s only
     // changes inact[s' > s]). Returns frontier < n (the reference then runs the
     // pinned G-check).
     __device__ __forceinline__ bool finish_iter() {
-        PBP_T0(tw);
-        LastWalk w;
-        walk_late(w);
-        PBP_T1(tw, 3);
-        PBP_T0(ta);
-        if (nce_ | w.cmask) apply_commits(w);
-        PBP_T1(ta, 4);
+        if constexpr (TM) {
+            LateTM w;
+            walk_tm(w);
+            int dinact = 0;
+            if (nce_) dinact = apply_commits(w);
+            if (w.cm) apply_tm(w, dinact);
+            if (lane < M) inact += dinact;
+            __syncwarp();
+        } else {
+            PBP_T0(tw);
+            LastWalk w;
+            walk_late(w);
+            PBP_T1(tw, 3);
+            PBP_T0(ta);
+            if (nce_ | w.cmask) {
+                const int dinact = apply_commits(w);
+                if (lane < M) inact += dinact;
+                __syncwarp();
+            }
+            PBP_T1(ta, 4);
+        }
         const int v = lane <= s_last_ ? (N >> 1) - inact : 0;
         act += __reduce_add_sync(kFull, v);
         return !done_;
@@ -833,7 +1004,8 @@ struct Dec {
     // event log. Commits of the early walk one after the other with the whole
     // warp (their blocks span lanes); last-pass commits one per lane (blocks
     // are disjoint, their L(S+1) are different arrays).
-    __device__ __forceinline__ void apply_commits(const LastWalk& w) {
+    template <class Walk>
+    __device__ __forceinline__ int apply_commits(const Walk& w) {
         constexpr uint32_t REGM = mask_of(0), SMEMM = mask_of(1);
         const int nce = nce_, fr_start = fr_start_;
         __syncwarp();
@@ -943,9 +1115,10 @@ struct Dec {
                 scatter(a->ev_xhat + ((long long)frame_ * a->ev_cap + nev) * NW, xbits, in_block, b, q, W, j0, start);
             ++nev;
         }
-        if (w.cmask) apply_last(w, nce, fr_start, dinact);
-        if (lane < M) inact += dinact;
-        __syncwarp();
+        if constexpr (!TM) {
+            if (w.cmask) apply_last(w, nce, fr_start, dinact);
+        }
+        return dinact;
     }
 
     // Last-pass commits (cmask bit t: stage SL + t), all inside the window:
