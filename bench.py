@@ -100,10 +100,13 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- CPU reference
 
-def cpu_reference_run(seconds_per_step=8.0, steps=1, warmup=0, want_threads=None):
+def cpu_reference_run(seconds_per_step=8.0, steps=1, warmup=0, want_threads=None, with_ref32=True):
     """The reference's own CPU decoder (oracle/_ref = reference sources compiled in place,
     fp64 as shipped) over a bounded sample of the config-2 sweep, all host threads.
-    Falls back to the C restatement (kind "port") when the reference build is absent."""
+    Falls back to the C restatement (kind "port") when the reference build is absent.
+    Like the stock decode_trial without --trace (sim_harness.cpp:84-90), no FreezeEvent
+    list is recorded. with_ref32: the same sources compiled with double -> float (the
+    GPU's arithmetic) timed on the same sample and reported beside it."""
     import oracle as O
     threads = want_threads or os.cpu_count() or 1
     kind = "reference" if O.REF is not None else "port"
@@ -111,43 +114,55 @@ def cpu_reference_run(seconds_per_step=8.0, steps=1, warmup=0, want_threads=None
     fz = O.construct(N, K, Z0, lib=lib)
     # calibrate: frames per SNR point so one step takes ~seconds_per_step
     per_point = max(2, threads // 2)
-    samples = {}
 
     def make(per):
         out = []
-        for i, snr in enumerate(SNRS):
+        for snr in SNRS:
             _, llr = O.trials(SEED, 0, per, fz, snr, lib=lib, threads=threads)
             out.append(llr)
         return out
 
+    def decode_all(llrs, prec):
+        pe = 0
+        for llr in llrs:
+            r = O.decode_batch("csfg", fz, llr, ALPHA, MAX_ITER, prec=prec, lib=lib, threads=threads,
+                               want_u=False, want_events=False)
+            pe += int(r["pe"].sum())
+        return pe
+
     llrs = make(per_point)
     t0 = time.perf_counter()
-    for llr in llrs:
-        O.decode_batch("csfg", fz, llr, ALPHA, MAX_ITER, prec=64, lib=lib, threads=threads, want_u=False)
+    decode_all(llrs, 64)
     dt = time.perf_counter() - t0
     per_point = max(per_point, int(per_point * seconds_per_step / max(dt, 1e-3)))
     llrs = make(per_point)
     frames = per_point * len(SNRS)
-    times = []
-    pe_total = 0
-    for it in range(warmup + steps):
-        t0 = time.perf_counter()
-        pe = 0
-        for llr in llrs:
-            r = O.decode_batch("csfg", fz, llr, ALPHA, MAX_ITER, prec=64, lib=lib, threads=threads,
-                               want_u=False)
-            pe += int(r["pe"].sum())
-        dt = time.perf_counter() - t0
-        if it >= warmup:
-            times.append(dt)
-            pe_total += pe
-    tot = sum(times)
-    bits_per_s = frames * K * len(times) / tot
-    return {"value": bits_per_s, "unit": "info bits/s", "cores": threads, "kind": kind,
-            "frames_per_step": frames, "seconds": tot, "ms_per_step": 1e3 * tot / len(times),
-            "pe_per_s": pe_total / tot,
-            "sample": f"{per_point} frames x {len(SNRS)} Eb/N0 points (trials 0..{per_point - 1}, seed {SEED}) "
-                      f"of config 2, fp64 reference decode_csfg, {threads} threads, LLRs pre-generated"}
+
+    def timed(prec):
+        times, pe_total = [], 0
+        for it in range(warmup + steps):
+            t0 = time.perf_counter()
+            pe = decode_all(llrs, prec)
+            dt = time.perf_counter() - t0
+            if it >= warmup:
+                times.append(dt)
+                pe_total += pe
+        tot = sum(times)
+        return frames * K * len(times) / tot, tot, pe_total
+
+    v64, tot, pe_total = timed(64)
+    out = {"value": v64, "unit": "info bits/s", "cores": threads, "kind": kind,
+           "frames_per_step": frames, "seconds": tot, "ms_per_step": 1e3 * tot / steps,
+           "pe_per_s": pe_total / tot,
+           "sample": f"{per_point} frames x {len(SNRS)} Eb/N0 points (trials 0..{per_point - 1}, seed {SEED}) "
+                     f"of config 2, fp64 reference decode_csfg (no event list), {threads} threads, "
+                     "LLRs pre-generated"}
+    if with_ref32 and kind == "reference":
+        v32, tot32, pe32 = timed(32)
+        out["ref32"] = {"value": v32, "unit": "info bits/s", "pe_per_s": pe32 / tot32,
+                        "what": "the same reference sources compiled with double -> float (the GPU's "
+                                "operation order and precision), same sample and threads"}
+    return out
 
 
 def dram_traffic(frames_per_launch):
@@ -175,6 +190,33 @@ def cpu_model():
     return "unknown"
 
 
+# --------------------------------------------------------------------------- launch
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_command(argv, gpus, port):
+    """torchrun command that runs this script on `gpus` ranks of one node (127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def relaunch_if_needed(args, argv):
+    """`bench.py --gpus N` outside torchrun: start N ranks (one process per GPU) and exit
+    with their status. Inside torchrun (WORLD_SIZE set) nothing happens."""
+    if os.environ.get("WORLD_SIZE") or args.gpus <= 1:
+        return
+    cmd = launch_command(argv, args.gpus, free_port())
+    log("bench: launching", " ".join(cmd))
+    sys.exit(subprocess.call(cmd))
+
+
 # --------------------------------------------------------------------------- GPU arm
 
 def main():
@@ -186,7 +228,9 @@ def main():
     ap.add_argument("--frames", type=int, default=FRAMES_PER_POINT)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-gen", action="store_true", help="skip the generate+decode figure")
     args = ap.parse_args()
+    relaunch_if_needed(args, sys.argv[1:])
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -205,7 +249,7 @@ def main():
                                        "(bounded CPU sample)", "decoder": "csfg", "max_iter": MAX_ITER,
                            "alpha": ALPHA, "cpu": cpu_model()},
                 "cpu_baseline": {"value": r["value"], "unit": "info bits/s", "cores": r["cores"],
-                                 "kind": r["kind"], "sample": r["sample"]},
+                                 "kind": r["kind"], "sample": r["sample"], "ref32": r.get("ref32")},
                 "e2e": {"value": r["value"], "unit": "info bits/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -214,11 +258,13 @@ def main():
     import torch
     import paper_1505_04979_b200 as P
 
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     dist = None
-    if world > 1:
+    if world > 1 or os.environ.get("TORCHELASTIC_RUN_ID"):  # every torchrun launch, even 1 rank
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     ctx = P.Context(local_rank)
@@ -330,6 +376,43 @@ def main():
                                  "MEASURED_PEAKS.json); achieved from CUDA-event launch times"},
             "clocks": clocks}
 
+    # ---- generation + decode: the same trials generated on the device inside the timed
+    #      region (pbp_simulate_point_device: decode_trial's channel + decode, counters) ----
+    if not args.no_gen:
+        gcnt = torch.zeros((len(SNRS), 10), dtype=torch.int64, device=dev)
+
+        def gen_step():
+            gcnt.zero_()
+            for i, snr in enumerate(SNRS):
+                P._check(P.lib.pbp_simulate_point_device(ctx.handle, C.byref(cs), 2, C.c_uint64(SEED), first,
+                                                         frames, snr, 0, ALPHA, MAX_ITER,
+                                                         P._abi.i64p(gcnt[i].data_ptr()), None))
+            if dist:
+                dist.all_reduce(gcnt)
+
+        with torch.cuda.stream(stream):
+            gen_step()  # staging allocation, warm
+            torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(args.steps):
+                gen_step()
+            g1.record(stream)
+            torch.cuda.synchronize()
+            gen_ms = g0.elapsed_time(g1)
+        if dist:
+            tt = torch.tensor([gen_ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            gen_ms = float(tt.item())
+        same = bool(torch.equal(gcnt.cpu(), torch.from_numpy(tot)))
+        line["gen_decode"] = {"value": total_frames * K * steps / (gen_ms / 1e3), "unit": "info bits/s",
+                              "ms_per_step": gen_ms / steps, "counters_equal_decode_only": same,
+                              "what": "pbp_simulate_point_device per Eb/N0 point: the reference's seeded "
+                                      "TrialRng/encode/AWGN frames generated on the device and decoded, "
+                                      "both inside the timed region (device time, max over ranks)"}
+
     # ---- e2e through the host-buffer C ABI (pinned host LLRs in, results out) ----
     if not args.no_e2e and rank == 0 or (not args.no_e2e and world > 1):
         # the whole sweep (every Eb/N0 point's frames) in one host-buffer call;
@@ -385,9 +468,10 @@ def main():
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            r = cpu_reference_run(seconds_per_step=12.0, steps=1, warmup=0)
+            r = cpu_reference_run(seconds_per_step=8.0, steps=1, warmup=0)
             line["cpu_baseline"] = {"value": r["value"], "unit": "info bits/s", "cores": r["cores"],
-                                    "kind": r["kind"], "sample": r["sample"], "cpu": cpu_model()}
+                                    "kind": r["kind"], "sample": r["sample"], "cpu": cpu_model(),
+                                    "ref32": r.get("ref32")}
         except Exception as e:  # reported, never fatal
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:

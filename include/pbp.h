@@ -199,6 +199,29 @@ int pbp_decode_count_device(pbp_ctx* ctx, const pbp_code* code, int decoder,
                             const float* llrs_dev, const uint32_t* u_dev, int64_t frames,
                             float alpha, int32_t max_iter, int64_t* counters_dev, void* stream);
 
+/* run_point's batches (src/sim_harness.cpp:136-178, kBatchSize = 256 at :21): trials
+ * [first_trial, first_trial + frames) generated and decoded as pbp_simulate_point does
+ * (fp64 != 0: the reference's double LLRs decoded in double), with ONE counter set per
+ * `batch` consecutive trials, so the caller can apply the reference's stop rule on batch
+ * boundaries. counters_out (host) receives ceil(frames / batch) x 10 int64 in the
+ * pbp_counters field order. */
+int pbp_simulate_batches(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed,
+                         int64_t first_trial, int64_t frames, int32_t batch, double ebn0_db,
+                         int noiseless, double alpha, int32_t max_iter, int fp64,
+                         int64_t* counters_out);
+
+/* Fixed-count Monte-Carlo sweep over several GPUs of one process (run_sweep with
+ * min_frame_errors = infinity, src/sim_harness.cpp:129-196, whose workers split the
+ * trials at :144-161): every point's trials [0, frames_per_point) are split into ndev
+ * contiguous ranges, one host thread per device generates and decodes its range, and
+ * the per-device counters (npoints x 10 int64) are summed in place with ONE
+ * ncclAllReduce(int64, sum) over NVLink/NVSwitch (libnccl.so.2, loaded at first use).
+ * Integer sums: the result equals the single-GPU and CPU aggregates. out: npoints sets. */
+int pbp_simulate_sweep_multi(const int* devices, int ndev, const pbp_code* code, int decoder,
+                             uint64_t seed, int64_t frames_per_point, const double* ebn0_db,
+                             int npoints, int noiseless, float alpha, int32_t max_iter,
+                             pbp_counters* out);
+
 /* Which kernel serves a code length: 1 = warp-resident fast path
  * (n = 128..1024), 2 = CTA-per-frame register-pass path (n = 2048..16384),
  * 0 = the generic kernel only. For tests and bench introspection. */

@@ -154,8 +154,11 @@ def decode(kind, frozen, llr, alpha=0.9375, max_iter=40, prec=32, lib=None, ev_c
 
 
 def decode_batch(kind, frozen, llr, alpha=0.9375, max_iter=40, prec=32, lib=None,
-                 threads=None, want_u=True):
-    """Batched oracle decode (frames x n). Returns dict of per-frame arrays."""
+                 threads=None, want_u=True, want_events=True):
+    """Batched oracle decode (frames x n). Returns dict of per-frame arrays.
+    want_events=False passes no event counter, so csfg records no FreezeEvent
+    list (the reference's decode_trial does that only with --trace,
+    sim_harness.cpp:84-90); "n_events" is then None."""
     lib = lib or C
     llr = np.ascontiguousarray(llr, np.float32 if prec == 32 else np.float64)
     frames, n = llr.shape
@@ -166,7 +169,7 @@ def decode_batch(kind, frozen, llr, alpha=0.9375, max_iter=40, prec=32, lib=None
     u = np.zeros((frames, n), np.uint8) if want_u else None
     it = np.zeros(frames, np.int32)
     sp = np.zeros(frames, np.int32)
-    ne = np.zeros(frames, np.int32)
+    ne = np.zeros(frames, np.int32) if want_events else None
     pe = np.zeros(frames, np.int64)
     rc = fn(KIND.get(kind, kind), n, _p(np.ascontiguousarray(frozen, np.uint8), _u8p),
             _p(llr, _f32p if prec == 32 else _f64p), frames, alpha, max_iter,

@@ -27,7 +27,8 @@ __all__ = [
     "PolarCode", "Codeword", "DecodeOutcome", "FreezeEvent", "PointStats", "SimConfig",
     "StopReason", "DecoderKind", "polar_transform", "encode", "extract_info_bits",
     "noise_variance", "bhattacharyya_profile", "decode_baseline", "decode_gmatrix",
-    "decode_csfg", "decode_batch", "generate", "simulate_point", "run_point", "run_sweep",
+    "decode_csfg", "decode_batch", "generate", "simulate_point", "simulate_batches", "simulate_sweep_multi",
+    "run_point", "run_sweep",
     "Context", "default_context", "LLR_CAP", "lib",
 ]
 
@@ -315,7 +316,7 @@ def _decode_one(code: PolarCode, kind: int, llrs, alpha, max_iter, events=None, 
     llr = np.ascontiguousarray(np.asarray(llrs, dtype=np.float64 if f64 else np.float32).reshape(-1))
     if llr.size != code.n:
         raise ValueError("init_state: LLR length != n")
-    cap = 4096
+    cap = max(1, int(max_iter) * code.m)  # one commit per stage per iteration at most: never truncated
     u = np.zeros(code.n, np.uint8)
     ev = np.zeros(cap * 5, np.int32)
     it, sp, ne = C.c_int32(), C.c_int32(), C.c_int32()
@@ -393,6 +394,45 @@ def simulate_point(code: PolarCode, decoder, seed: int, first_trial: int, frames
     return dict(zip(COUNTER_FIELDS, [int(v) for v in vals]))
 
 
+def simulate_batches(code: PolarCode, decoder, seed: int, first_trial: int, frames: int, ebn0_db: float,
+                     batch: int = 256, alpha: float = 0.9375, max_iter: int = 40, noiseless: bool = False,
+                     ctx=None, precision: str = "f32") -> np.ndarray:
+    """One counter set per `batch` consecutive trials (ceil(frames/batch) x 10 int64, the
+    COUNTER_FIELDS order): run_point's batches (sim_harness.cpp:136-178) on the device."""
+    ctx = ctx or default_context()
+    nb = (int(frames) + int(batch) - 1) // int(batch)
+    out = np.zeros((max(nb, 1), 10), np.int64)
+    cs = code.c_struct()
+    _check(lib.pbp_simulate_batches(ctx.handle, C.byref(cs), _kind(decoder), C.c_uint64(seed), int(first_trial),
+                                    int(frames), int(batch), float(ebn0_db), int(bool(noiseless)), float(alpha),
+                                    int(max_iter), int(_precision(precision)), _abi.i64p(out)))
+    return out[:nb]
+
+
+def simulate_sweep_multi(code: PolarCode, decoder, seed: int, frames_per_point: int, snrs: Sequence[float],
+                         devices: Optional[Sequence[int]] = None, alpha: float = 0.9375, max_iter: int = 40,
+                         noiseless: bool = False) -> List[dict]:
+    """run_sweep's counters with fixed frame counts over several GPUs of this process
+    (pbp_simulate_sweep_multi: one host thread per device, contiguous trial ranges, one
+    NCCL int64 all-reduce). devices: default every visible GPU."""
+    devs = list(range(device_count())) if devices is None else [int(d) for d in devices]
+    if not devs:
+        raise RuntimeError("simulate_sweep_multi: no CUDA device")
+    dv = (C.c_int * len(devs))(*devs)
+    sv = (C.c_double * len(snrs))(*[float(x) for x in snrs])
+    out = (_abi.PbpCounters * len(snrs))()
+    cs = code.c_struct()
+    _check(lib.pbp_simulate_sweep_multi(dv, len(devs), C.byref(cs), _kind(decoder), C.c_uint64(seed),
+                                        int(frames_per_point), sv, len(snrs), int(bool(noiseless)), float(alpha),
+                                        int(max_iter), out))
+    rows = []
+    for c in out:
+        vals = [c.frames, c.bit_errors, c.frame_errors, c.sum_iters, c.sum_iters_sq, c.sum_pe,
+                c.sum_events, c.stop_hist[0], c.stop_hist[1], c.stop_hist[2]]
+        rows.append(dict(zip(COUNTER_FIELDS, [int(v) for v in vals])))
+    return rows
+
+
 @dataclass
 class SimConfig:
     """SimConfig (sim_harness.hpp:23-36)."""
@@ -454,36 +494,29 @@ K_BATCH = 256  # kBatchSize (sim_harness.cpp:21)
 def run_point(cfg: SimConfig, snr_db: float, ctx=None) -> List[PointStats]:
     """run_point (sim_harness.cpp:129-186) on the GPU, 256-frame batch stop rule included.
 
-    Whole batches are decoded on the device; the stop rule is evaluated on the same batch
-    boundaries as the reference, so the frame counts (and every sum) are identical."""
+    Chunks of whole batches are generated and decoded on the device, which returns one
+    counter set per 256-trial batch (pbp_simulate_batches); the batches are merged in trial
+    order and the stop rule is evaluated on the same boundaries as the reference, so the
+    frame counts (and every sum) are identical."""
     if not cfg.decoders:
         raise ValueError("run_point: no decoders")
     if cfg.max_frames < 1:
         raise ValueError("run_point: max_frames < 1")
     accs = [dict.fromkeys(COUNTER_FIELDS, 0) for _ in cfg.decoders]
     frames = 0
-    # grow the chunk while the stop rule cannot trigger, keeping batch alignment
-    chunk = K_BATCH
+    chunk = K_BATCH * 16
     while frames < cfg.max_frames:
-        todo = min(chunk, cfg.max_frames - frames)
-        # never cross the point where some decoder could first reach min_frame_errors:
-        # only whole batches are added, then the rule is re-checked per batch below
-        nb = (todo + K_BATCH - 1) // K_BATCH
-        added = 0
-        for b in range(nb):
-            batch = min(K_BATCH, cfg.max_frames - frames)
-            for d, kind in enumerate(cfg.decoders):
-                c = simulate_point(cfg.code, kind, cfg.seed, frames, batch, snr_db, cfg.alpha,
-                                   cfg.max_iter, cfg.noiseless, ctx, precision=cfg.precision)
-                for key in COUNTER_FIELDS:
-                    accs[d][key] += c[key]
-            frames += batch
-            added += batch
+        c = min(chunk, cfg.max_frames - frames)
+        per = [simulate_batches(cfg.code, kind, cfg.seed, frames, c, snr_db, K_BATCH, cfg.alpha, cfg.max_iter,
+                                cfg.noiseless, ctx, precision=cfg.precision) for kind in cfg.decoders]
+        for b in range(per[0].shape[0]):
+            for d in range(len(cfg.decoders)):
+                for i, key in enumerate(COUNTER_FIELDS):
+                    accs[d][key] += int(per[d][b, i])
             if all(a["frame_errors"] >= cfg.min_frame_errors for a in accs):
                 return [make_stats(cfg, kind, snr_db, a) for kind, a in zip(cfg.decoders, accs)]
-            if frames >= cfg.max_frames:
-                break
-        chunk = min(chunk * 2, 1 << 16)
+        frames += c
+        chunk = min(chunk * 2, K_BATCH * 1024)
     return [make_stats(cfg, kind, snr_db, a) for kind, a in zip(cfg.decoders, accs)]
 
 

@@ -685,14 +685,15 @@ struct Dec {
                 if (args.stop) args.stop[f] = (uint8_t)stop;
                 if (args.nev) args.nev[f] = nev;
                 if (args.counters) {
-                    atomicAdd(&args.counters[kCntFrames], 1ull);
-                    atomicAdd(&args.counters[kCntBitErr], (unsigned long long)be);
-                    atomicAdd(&args.counters[kCntFrameErr], be > 0 ? 1ull : 0ull);
-                    atomicAdd(&args.counters[kCntIters], (unsigned long long)iters);
-                    atomicAdd(&args.counters[kCntItersSq], (unsigned long long)iters * iters);
-                    atomicAdd(&args.counters[kCntPe], (unsigned long long)pe);
-                    atomicAdd(&args.counters[kCntEvents], (unsigned long long)nev);
-                    atomicAdd(&args.counters[kCntStop0 + stop], 1ull);
+                    unsigned long long* cs = counter_set(args, f);
+                    atomicAdd(&cs[kCntFrames], 1ull);
+                    atomicAdd(&cs[kCntBitErr], (unsigned long long)be);
+                    atomicAdd(&cs[kCntFrameErr], be > 0 ? 1ull : 0ull);
+                    atomicAdd(&cs[kCntIters], (unsigned long long)iters);
+                    atomicAdd(&cs[kCntItersSq], (unsigned long long)iters * iters);
+                    atomicAdd(&cs[kCntPe], (unsigned long long)pe);
+                    atomicAdd(&cs[kCntEvents], (unsigned long long)nev);
+                    atomicAdd(&cs[kCntStop0 + stop], 1ull);
                 }
             }
         }

@@ -334,14 +334,15 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
             if (a.stop) a.stop[frame] = (uint8_t)stop;
             if (a.nev) a.nev[frame] = s_nev;
             if (a.counters) {
-                atomicAdd(&a.counters[kCntFrames], 1ull);
-                atomicAdd(&a.counters[kCntBitErr], (unsigned long long)s_bit_err);
-                atomicAdd(&a.counters[kCntFrameErr], s_bit_err > 0 ? 1ull : 0ull);
-                atomicAdd(&a.counters[kCntIters], (unsigned long long)iters);
-                atomicAdd(&a.counters[kCntItersSq], (unsigned long long)iters * iters);
-                atomicAdd(&a.counters[kCntPe], (unsigned long long)pe);
-                atomicAdd(&a.counters[kCntEvents], (unsigned long long)s_nev);
-                atomicAdd(&a.counters[kCntStop0 + stop], 1ull);
+                unsigned long long* cs = counter_set(a, frame);
+                atomicAdd(&cs[kCntFrames], 1ull);
+                atomicAdd(&cs[kCntBitErr], (unsigned long long)s_bit_err);
+                atomicAdd(&cs[kCntFrameErr], s_bit_err > 0 ? 1ull : 0ull);
+                atomicAdd(&cs[kCntIters], (unsigned long long)iters);
+                atomicAdd(&cs[kCntItersSq], (unsigned long long)iters * iters);
+                atomicAdd(&cs[kCntPe], (unsigned long long)pe);
+                atomicAdd(&cs[kCntEvents], (unsigned long long)s_nev);
+                atomicAdd(&cs[kCntStop0 + stop], 1ull);
             }
         }
         __syncthreads();

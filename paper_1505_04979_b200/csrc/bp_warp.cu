@@ -1520,7 +1520,11 @@ struct Dec {
                 case kCntStop2: v = stop == 2; break;
                 default: break;
             }
-            if (lane < kNumCounters) sm->cnt[lane] += v;
+            if (args.cnt_batch > 0) {
+                if (lane < kNumCounters && v) atomicAdd(&counter_set(args, f)[lane], v);
+            } else if (lane < kNumCounters) {
+                sm->cnt[lane] += v;
+            }
         }
     }
 

@@ -195,6 +195,7 @@ struct DecodeReq {
     uint32_t* ev_xhat = nullptr;
     const uint32_t* truth = nullptr;
     unsigned long long* counters = nullptr;
+    int cnt_batch = 0;  // > 0: one counter set per cnt_batch frames (run_point batches)
     bool force_generic = false;
     // fast path: re-routed frames go to this list (indices + frame_base) and
     // the caller runs the generic pass later (run_generic_list)
@@ -304,6 +305,7 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
     a.ev_xhat = r.ev_xhat;
     a.truth_u = r.truth;
     a.counters = r.counters;
+    a.cnt_batch = r.cnt_batch;
     a.list_len = s.ctl.p + 2;
 
     // the warp kernel is fp32 only; fp64 decodes run the generic kernel on double
@@ -434,6 +436,9 @@ int run_generate(pbp_ctx* ctx, uint64_t seed, long long first, long long count, 
 cudaStream_t pick(pbp_ctx* ctx, void* s) { return s ? (cudaStream_t)s : ctx->stream; }
 
 }  // namespace
+
+// error text for the C ABI's other translation units (pbp_multi.cpp)
+__attribute__((visibility("hidden"))) int pbp_set_error(int status, const char* msg) { return fail(status, msg); }
 
 extern "C" {
 
@@ -980,6 +985,8 @@ int pbp_decode_count_device(pbp_ctx* ctx, const pbp_code* code, int decoder, con
                             const uint32_t* u_dev, int64_t frames, float alpha, int32_t max_iter,
                             int64_t* counters_dev, void* stream) {
     if (!ctx) return fail(PBP_EINVAL, "null context");
+    // the kernels read truth_u whenever counters are requested
+    if (!counters_dev || !u_dev) return fail(PBP_EINVAL, "pbp_decode_count_device: null counters or u");
     PBP_CUDA(cudaSetDevice(ctx->device));
     int rc = upload_code(ctx, code);
     if (rc) return rc;
@@ -999,7 +1006,8 @@ int pbp_decode_count_device(pbp_ctx* ctx, const pbp_code* code, int decoder, con
 // f64, the reference's double LLRs decoded in double.
 static int simulate_point_impl(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed,
                                int64_t first_trial, int64_t frames, double ebn0_db, int noiseless, double alpha,
-                               bool f64, int32_t max_iter, int64_t* counters_dev, void* stream) {
+                               bool f64, int32_t max_iter, int64_t* counters_dev, void* stream,
+                               int batch = 0) {
     if (!ctx) return fail(PBP_EINVAL, "null context");
     if (frames < 0) return fail(PBP_EINVAL, "frames < 0");
     PBP_CUDA(cudaSetDevice(ctx->device));
@@ -1008,7 +1016,8 @@ static int simulate_point_impl(pbp_ctx* ctx, const pbp_code* code, int decoder, 
     const int n = ctx->n, nw = (n + 31) / 32;
     // chunk so the staging stays bounded (512 MiB of fp32 LLRs: a config's 10^5-frame
     // point at n = 1024 is one chunk, so one decode tail per point)
-    const long long chunk = std::max<long long>(1, std::min<long long>(frames, (1ll << 27) / n));
+    long long chunk = std::max<long long>(1, std::min<long long>(frames, (1ll << 27) / n));
+    if (batch > 0 && chunk < frames) chunk = std::max<long long>(batch, chunk / batch * batch);  // whole batches
     // this call's slot: its generation staging and launch resources (an
     // asynchronous call may overlap other calls on other streams)
     DecodeSlot& sl = next_slot(ctx);
@@ -1034,7 +1043,9 @@ static int simulate_point_impl(pbp_ctx* ctx, const pbp_code* code, int decoder, 
         r.frames = c;
         r.max_iter = max_iter;
         r.truth = sl.gen_truth.p;
-        r.counters = reinterpret_cast<unsigned long long*>(counters_dev);
+        r.counters = reinterpret_cast<unsigned long long*>(counters_dev) +
+                     (batch > 0 ? (done / batch) * pbp::kNumCounters : 0);
+        r.cnt_batch = batch;
         if ((rc = run_decode(ctx, r, sl, st))) return rc;
     }
     return PBP_OK;
@@ -1084,6 +1095,27 @@ int pbp_simulate_point_f64(pbp_ctx* ctx, const pbp_code* code, int decoder, uint
                            pbp_counters* out) {
     return simulate_point_host(ctx, code, decoder, seed, first_trial, frames, ebn0_db, noiseless, alpha, true,
                                max_iter, out);
+}
+
+int pbp_simulate_batches(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed, int64_t first_trial,
+                         int64_t frames, int32_t batch, double ebn0_db, int noiseless, double alpha,
+                         int32_t max_iter, int fp64, int64_t* counters_out) {
+    if (!ctx || !counters_out) return fail(PBP_EINVAL, "null argument");
+    if (batch < 1) return fail(PBP_EINVAL, "pbp_simulate_batches: batch < 1");
+    if (frames < 0) return fail(PBP_EINVAL, "frames < 0");
+    if (decoder < 0 || decoder > 2) return fail(PBP_EINVAL, "unknown decoder kind");
+    PBP_CUDA(cudaSetDevice(ctx->device));
+    const long long nb = (frames + batch - 1) / batch;
+    int rc;
+    if ((rc = ctx->counters.ensure((size_t)std::max<long long>(nb, 1) * pbp::kNumCounters))) return rc;
+    PBP_CUDA(cudaMemsetAsync(ctx->counters.p, 0, (size_t)nb * pbp::kNumCounters * 8, ctx->stream));
+    rc = simulate_point_impl(ctx, code, decoder, seed, first_trial, frames, ebn0_db, noiseless, alpha, fp64 != 0,
+                             max_iter, reinterpret_cast<int64_t*>(ctx->counters.p), ctx->stream, batch);
+    if (rc) return rc;
+    PBP_CUDA(cudaMemcpyAsync(counters_out, ctx->counters.p, (size_t)nb * pbp::kNumCounters * 8,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    PBP_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PBP_OK;
 }
 
 }  // extern "C"

@@ -44,7 +44,8 @@ struct DecodeArgs {
     uint32_t* ev_xhat;
     // counters mode (nullable)
     const uint32_t* truth_u;          // frames x ceil(n/32)
-    unsigned long long* counters;     // kNumCounters
+    unsigned long long* counters;     // kNumCounters (cnt_batch > 0: one set per cnt_batch frames)
+    int cnt_batch;                    // 0: one counter set; > 0: set f / cnt_batch for frame f
     // work distribution
     unsigned long long* queue;        // atomic frame counter (zeroed before launch)
     // re-route list: the fast kernel appends frames it cannot take; the
@@ -72,6 +73,12 @@ struct GenArgs {
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// counter set of frame f (its run_point batch when the caller asked for
+// per-batch sums: the host applies the reference's stop rule on them)
+__device__ __forceinline__ unsigned long long* counter_set(const DecodeArgs& a, long long f) {
+    return a.cnt_batch > 0 ? a.counters + (f / a.cnt_batch) * kNumCounters : a.counters;
+}
 
 // XOR butterfly of the polar transform (polar_code.cpp:13-20) restricted to
 // bit positions h < nbits inside one 32-bit word: bit i (with i&h == 0)

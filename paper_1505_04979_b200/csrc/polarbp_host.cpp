@@ -4,6 +4,7 @@
 // construction, file formats, the per-trial host RNG and report formatting are
 // host utilities, as in the reference.
 #include <algorithm>
+#include <charconv>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -14,6 +15,8 @@
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "pbp.h"
 #include "polarbp/bp_core.hpp"
@@ -338,7 +341,8 @@ DecodeOutcome one_frame(const PolarCode& code, int kind, std::span<const T> llrs
     out.u_hat.assign(code.n, 0);
     int32_t it = 0, stop = 0, nev = 0;
     int64_t pe = 0;
-    const int cap = 4096, nw = (code.n + 31) / 32;
+    // at most one commit per stage per iteration (csfg_freeze.cpp:111-118): never truncated
+    const int cap = std::max(1, max_iter * code.m), nw = (code.n + 31) / 32;
     std::vector<int32_t> ev(events ? static_cast<size_t>(cap) * 5 : 5);
     std::vector<uint32_t> xw(events ? static_cast<size_t>(cap) * nw : 0);  // each event's x_hat
     uint32_t* xp = events ? xw.data() : nullptr;
@@ -494,77 +498,150 @@ PointStats stats_of(const SimConfig& cfg, DecoderKind kind, double snr, const Ac
 
 }  // namespace
 
+namespace {
+
+// one context per visible device for one run_point call (pbp_ctx is not
+// thread-safe: each worker thread drives its own device's context)
+struct DevicePool {
+    std::vector<pbp_ctx*> ctx;
+    explicit DevicePool(int want) {
+        const int n = std::max(1, std::min(want, pbp_device_count()));
+        for (int d = 0; d < n; ++d) {
+            pbp_ctx* c = nullptr;
+            const int rc = pbp_ctx_create(d, &c);
+            if (rc) {
+                this->~DevicePool();
+                raise(rc);
+            }
+            ctx.push_back(c);
+        }
+    }
+    ~DevicePool() {
+        for (pbp_ctx* c : ctx)
+            if (c) pbp_ctx_destroy(c);
+        ctx.clear();
+    }
+};
+
+void add_batch(Acc& a, const std::int64_t* c) {
+    a.frames += c[0];
+    a.bit_errors += c[1];
+    a.frame_errors += c[2];
+    a.sum_iters += c[3];
+    a.sum_iters_sq += c[4];
+    a.sum_pe += c[5];
+}
+
+}  // namespace
+
+// run_point (sim_harness.cpp:129-186). Without a trace sink the trials are
+// generated and decoded on the GPUs, which return one int64 counter set per
+// 256-trial batch (pbp_simulate_batches); chunks of whole batches are split
+// into contiguous per-device ranges (one host thread per visible GPU), and
+// the batches are merged in trial order with the stop rule checked at every
+// batch boundary, as in the reference -- so the rows are identical for any
+// device count. With a trace sink (single device, as the reference forces one
+// worker) each 256-trial batch is decoded frame by frame with its freeze
+// events, and events are emitted only for the batches that are merged.
 std::vector<PointStats> run_point(const SimConfig& cfg, double snr_db, const TraceSink* trace) {
     if (cfg.decoders.empty()) throw std::invalid_argument("run_point: no decoders");
     if (cfg.max_frames < 1) throw std::invalid_argument("run_point: max_frames < 1");
     constexpr long long kBatch = 256;  // stop rule granularity (sim_harness.cpp:21)
     const PolarCode& code = cfg.code;
-    const ChannelConfig ch{snr_db, static_cast<double>(code.k) / code.n, cfg.noiseless};
     const size_t nd = cfg.decoders.size();
     std::vector<Acc> acc(nd);
+    auto finish = [&]() {
+        std::vector<PointStats> rows;
+        for (size_t d = 0; d < nd; ++d) rows.push_back(stats_of(cfg, cfg.decoders[d], snr_db, acc[d]));
+        return rows;
+    };
+    auto enough = [&]() {
+        for (const Acc& a : acc)
+            if (a.frame_errors < cfg.min_frame_errors) return false;
+        return true;
+    };
     long long frames = 0;
-    long long chunk = kBatch * 16;
-    while (frames < cfg.max_frames) {
-        const long long c = std::min(chunk, cfg.max_frames - frames);
-        std::vector<float> llr;
-        std::vector<double> llr64;
-        std::vector<Bits> u;
-        if (cfg.fp64)
-            generate_frames(code, cfg.seed, frames, c, ch, llr64, &u);
-        else
-            generate_frames(code, cfg.seed, frames, c, ch, llr, &u);
-        std::vector<std::vector<DecodeOutcome>> outs(nd);
-        for (size_t d = 0; d < nd; ++d) {
-            const auto kind = static_cast<BatchDecoder>(cfg.decoders[d]);
-            if (trace && cfg.decoders[d] == DecoderKind::csfg) {
-                for (long long f = 0; f < c; ++f) {
-                    std::vector<FreezeEvent> ev;
-                    if (cfg.fp64)
-                        outs[d].push_back(one_frame<double>(
-                            code, PBP_CSFG, std::span<const double>(llr64.data() + f * code.n, code.n), cfg.alpha,
-                            cfg.max_iter, &ev));
-                    else
-                        outs[d].push_back(one_frame<float>(
-                            code, PBP_CSFG, std::span<const float>(llr.data() + f * code.n, code.n), cfg.alpha,
-                            cfg.max_iter, &ev));
-                    for (const auto& e : ev) (*trace)(frames + f, e);
-                }
-            } else if (cfg.fp64) {
-                outs[d] = decode_batch(code, kind, std::span<const double>(llr64), cfg.alpha, cfg.max_iter);
-            } else {
-                outs[d] = decode_batch(code, kind, std::span<const float>(llr), cfg.alpha, cfg.max_iter);
-            }
-        }
-        // merge in trial order, stop rule on 256-frame batch boundaries
-        for (long long b0 = 0; b0 < c; b0 += kBatch) {
-            const long long b1 = std::min(c, b0 + kBatch);
-            for (long long f = b0; f < b1; ++f)
+    if (trace) {
+        const ChannelConfig ch{snr_db, static_cast<double>(code.k) / code.n, cfg.noiseless};
+        while (frames < cfg.max_frames) {
+            const long long c = std::min(kBatch, cfg.max_frames - frames);
+            std::vector<float> llr;
+            std::vector<double> llr64;
+            std::vector<Bits> u;
+            if (cfg.fp64)
+                generate_frames(code, cfg.seed, frames, c, ch, llr64, &u);
+            else
+                generate_frames(code, cfg.seed, frames, c, ch, llr, &u);
+            for (long long f = 0; f < c; ++f)
                 for (size_t d = 0; d < nd; ++d) {
-                    const DecodeOutcome& o = outs[d][f];
+                    const int kind = static_cast<int>(cfg.decoders[d]);
+                    std::vector<FreezeEvent> ev;
+                    std::vector<FreezeEvent>* evp = cfg.decoders[d] == DecoderKind::csfg ? &ev : nullptr;
+                    const DecodeOutcome o =
+                        cfg.fp64 ? one_frame<double>(code, kind, std::span<const double>(llr64.data() + f * code.n, code.n),
+                                                     cfg.alpha, cfg.max_iter, evp)
+                                 : one_frame<float>(code, kind, std::span<const float>(llr.data() + f * code.n, code.n),
+                                                    cfg.alpha, cfg.max_iter, evp);
+                    for (const auto& e : ev) (*trace)(frames + f, e);
                     long long be = 0;
                     for (int r = 0; r < code.n; ++r)
                         if (!code.frozen[r] && o.u_hat[r] != u[f][r]) ++be;
-                    acc[d].frames += 1;
-                    acc[d].bit_errors += be;
-                    acc[d].frame_errors += be > 0;
-                    acc[d].sum_iters += o.iterations_used;
-                    acc[d].sum_iters_sq += static_cast<long long>(o.iterations_used) * o.iterations_used;
-                    acc[d].sum_pe += o.pe_activations;
+                    const std::int64_t cell[6] = {1, be, be > 0, o.iterations_used,
+                                                  static_cast<long long>(o.iterations_used) * o.iterations_used,
+                                                  o.pe_activations};
+                    add_batch(acc[d], cell);
                 }
-            bool enough = true;
-            for (const Acc& a : acc) enough = enough && a.frame_errors >= cfg.min_frame_errors;
-            if (enough) {
-                std::vector<PointStats> rows;
-                for (size_t d = 0; d < nd; ++d) rows.push_back(stats_of(cfg, cfg.decoders[d], snr_db, acc[d]));
-                return rows;
+            frames += c;
+            if (enough()) break;
+        }
+        return finish();
+    }
+    DevicePool pool(pbp_device_count());
+    const int ng = static_cast<int>(pool.ctx.size());
+    const pbp_code cv = view(code);
+    long long chunk = kBatch * 16;
+    std::vector<std::int64_t> cnt;
+    while (frames < cfg.max_frames) {
+        const long long c = std::min(chunk, cfg.max_frames - frames);
+        const long long nb = (c + kBatch - 1) / kBatch;
+        cnt.assign(static_cast<size_t>(nd * nb * 10), 0);
+        // device g takes batches [nb*g/ng, nb*(g+1)/ng) of every decoder
+        std::vector<int> rcs(ng, PBP_OK);
+        std::vector<std::string> errs(ng);
+        auto work = [&](int g) {
+            const long long b0 = nb * g / ng, b1 = nb * (g + 1) / ng;
+            if (b1 <= b0) return;
+            const long long first = frames + b0 * kBatch;
+            const long long count = std::min(c, b1 * kBatch) - b0 * kBatch;
+            for (size_t d = 0; d < nd && !rcs[g]; ++d) {
+                rcs[g] = pbp_simulate_batches(pool.ctx[g], &cv, static_cast<int>(cfg.decoders[d]), cfg.seed, first,
+                                              count, static_cast<int32_t>(kBatch), snr_db, cfg.noiseless ? 1 : 0,
+                                              cfg.alpha, cfg.max_iter, cfg.fp64 ? 1 : 0,
+                                              cnt.data() + (d * nb + b0) * 10);
+                if (rcs[g]) errs[g] = pbp_last_error();
             }
+        };
+        if (ng == 1) {
+            work(0);
+        } else {
+            std::vector<std::thread> th;
+            for (int g = 0; g < ng; ++g) th.emplace_back(work, g);
+            for (auto& t : th) t.join();
+        }
+        for (int g = 0; g < ng; ++g)
+            if (rcs[g]) {
+                if (rcs[g] == PBP_EINVAL) throw std::invalid_argument(errs[g]);
+                throw std::runtime_error(errs[g]);
+            }
+        // merge in trial order, stop rule on 256-frame batch boundaries
+        for (long long b = 0; b < nb; ++b) {
+            for (size_t d = 0; d < nd; ++d) add_batch(acc[d], cnt.data() + (d * nb + b) * 10);
+            if (enough()) return finish();
         }
         frames += c;
         chunk = std::min(chunk * 2, kBatch * 1024);
     }
-    std::vector<PointStats> rows;
-    for (size_t d = 0; d < nd; ++d) rows.push_back(stats_of(cfg, cfg.decoders[d], snr_db, acc[d]));
-    return rows;
+    return finish();
 }
 
 std::vector<PointStats> run_sweep(const SimConfig& cfg, const TraceSink* trace) {
@@ -626,37 +703,162 @@ std::vector<PointStats> parse_results_csv(const std::string& text) {
     return rows;
 }
 
-std::string results_json(const SimConfig& cfg, std::span<const PointStats> rows) {
-    // a plain writer (the reference uses nlohmann::json::dump(2))
-    std::ostringstream o;
-    auto num = [](double v) {
-        char b[64];
-        std::snprintf(b, sizeof(b), "%.17g", v);
-        return std::string(b);
-    };
-    o << "{\n  \"config\": {\n    \"n\": " << cfg.code.n << ",\n    \"k\": " << cfg.code.k << ",\n    \"frozen\": [";
-    const auto fp = cfg.code.frozen_positions();
-    for (size_t i = 0; i < fp.size(); ++i) o << (i ? ", " : "") << fp[i] + 1;
-    o << "],\n    \"code_source\": \"" << cfg.code_source << "\",\n    \"decoders\": [";
-    for (size_t i = 0; i < cfg.decoders.size(); ++i) o << (i ? ", " : "") << '"' << to_string(cfg.decoders[i]) << '"';
-    o << "],\n    \"snr_db\": [";
-    for (size_t i = 0; i < cfg.snr_db.size(); ++i) o << (i ? ", " : "") << num(cfg.snr_db[i]);
-    o << "],\n    \"alpha\": " << num(cfg.alpha) << ",\n    \"max_iter\": " << cfg.max_iter
-      << ",\n    \"min_frame_errors\": " << cfg.min_frame_errors << ",\n    \"max_frames\": " << cfg.max_frames
-      << ",\n    \"seed\": " << cfg.seed << ",\n    \"workers\": " << cfg.workers
-      << ",\n    \"noiseless\": " << (cfg.noiseless ? "true" : "false") << "\n  },\n  \"results\": [";
-    for (size_t i = 0; i < rows.size(); ++i) {
-        const auto& r = rows[i];
-        o << (i ? "," : "") << "\n    {\"decoder\": \"" << to_string(r.decoder) << "\", \"snr_db\": " << num(r.snr_db)
-          << ", \"frames\": " << r.frames << ", \"bit_errors\": " << r.bit_errors
-          << ", \"frame_errors\": " << r.frame_errors << ", \"ber\": " << num(r.ber) << ", \"fer\": " << num(r.fer)
-          << ", \"fer_ci95\": " << num(r.fer_ci95) << ", \"avg_iters\": " << num(r.avg_iters)
-          << ", \"iters_ci95\": " << num(r.iters_ci95) << ", \"avg_pe_activations\": " << num(r.avg_pe_activations)
-          << ", \"norm_computations\": " << num(r.norm_computations)
-          << ", \"low_confidence\": " << (r.low_confidence ? "true" : "false") << "}";
+namespace {
+
+// A JSON value in the form nlohmann::json::dump(2) prints it (the reference's
+// writer, sim_harness.cpp:250-289): objects are std::map-ordered (sorted
+// keys), every array element and object member on its own line indented by 2
+// per level, "key": value, empty containers as [] / {}, integers as-is,
+// booleans true/false, doubles as the shortest round-trip digits laid out
+// like nlohmann's format_buffer (fixed for decimal exponents -4 < n <= 15,
+// with ".0" appended to integral values; else d[.igits]e+XX).
+struct Json {
+    enum Kind { kObj, kArr, kStr, kRaw } kind = kRaw;
+    std::string text;                                // kStr / kRaw
+    std::vector<std::pair<std::string, Json>> items; // kObj (key order fixed below) / kArr (key unused)
+};
+
+std::string json_double(double v) {
+    if (!std::isfinite(v)) return "null";
+    if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
+    char buf[64];
+    const auto res = std::to_chars(buf, buf + sizeof(buf), v, std::chars_format::scientific);
+    // digits d.ddddde[+-]x -> digit string and decimal exponent of the last digit
+    std::string sci(buf, res.ptr);
+    std::string sign;
+    if (sci[0] == '-') {
+        sign = "-";
+        sci.erase(0, 1);
     }
-    o << "\n  ]\n}\n";
-    return o.str();
+    const size_t epos = sci.find('e');
+    const int e10 = std::atoi(sci.c_str() + epos + 1);
+    std::string digits;
+    for (size_t i = 0; i < epos; ++i)
+        if (sci[i] != '.') digits += sci[i];
+    while (digits.size() > 1 && digits.back() == '0') digits.pop_back();
+    const int k = static_cast<int>(digits.size());
+    const int n = e10 + 1;  // decimal point position
+    std::string out;
+    if (k <= n && n <= 15) {
+        out = digits + std::string(n - k, '0') + ".0";
+    } else if (0 < n && n <= 15) {
+        out = digits.substr(0, n) + "." + digits.substr(n);
+    } else if (-4 < n && n <= 0) {
+        out = "0." + std::string(-n, '0') + digits;
+    } else {
+        out = digits.substr(0, 1);
+        if (k > 1) out += "." + digits.substr(1);
+        const int x = n - 1;
+        char eb[16];
+        std::snprintf(eb, sizeof(eb), "e%c%02d", x < 0 ? '-' : '+', x < 0 ? -x : x);
+        out += eb;
+    }
+    return sign + out;
+}
+
+std::string json_escape(const std::string& s) {
+    std::string o = "\"";
+    for (unsigned char c : s) {
+        switch (c) {
+            case '"': o += "\\\""; break;
+            case '\\': o += "\\\\"; break;
+            case '\b': o += "\\b"; break;
+            case '\f': o += "\\f"; break;
+            case '\n': o += "\\n"; break;
+            case '\r': o += "\\r"; break;
+            case '\t': o += "\\t"; break;
+            default:
+                if (c < 0x20) {
+                    char b[8];
+                    std::snprintf(b, sizeof(b), "\\u%04x", c);
+                    o += b;
+                } else {
+                    o += static_cast<char>(c);
+                }
+        }
+    }
+    return o + "\"";
+}
+
+Json jraw(std::string t) { return Json{Json::kRaw, std::move(t), {}}; }
+Json jstr(const std::string& t) { return Json{Json::kStr, json_escape(t), {}}; }
+Json jnum(double v) { return jraw(json_double(v)); }
+template <class I>
+Json jint(I v) { return jraw(std::to_string(v)); }
+Json jbool(bool v) { return jraw(v ? "true" : "false"); }
+Json jobj(std::vector<std::pair<std::string, Json>> m) {
+    std::sort(m.begin(), m.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    return Json{Json::kObj, "", std::move(m)};
+}
+Json jarr(std::vector<Json> v) {
+    Json j{Json::kArr, "", {}};
+    for (auto& x : v) j.items.emplace_back("", std::move(x));
+    return j;
+}
+
+void dump2(const Json& j, int depth, std::string& o) {
+    if (j.kind == Json::kRaw || j.kind == Json::kStr) {
+        o += j.text;
+        return;
+    }
+    const char open = j.kind == Json::kObj ? '{' : '[', close = j.kind == Json::kObj ? '}' : ']';
+    if (j.items.empty()) {
+        o += open;
+        o += close;
+        return;
+    }
+    o += open;
+    o += '\n';
+    const std::string ind(2 * (depth + 1), ' ');
+    for (size_t i = 0; i < j.items.size(); ++i) {
+        o += ind;
+        if (j.kind == Json::kObj) o += json_escape(j.items[i].first) + ": ";
+        dump2(j.items[i].second, depth + 1, o);
+        if (i + 1 < j.items.size()) o += ',';
+        o += '\n';
+    }
+    o += std::string(2 * depth, ' ');
+    o += close;
+}
+
+}  // namespace
+
+std::string results_json(const SimConfig& cfg, std::span<const PointStats> rows) {
+    std::vector<Json> frozen, decoders, snrs, results;
+    for (int pos : cfg.code.frozen_positions()) frozen.push_back(jint(pos + 1));
+    for (DecoderKind d : cfg.decoders) decoders.push_back(jstr(to_string(d)));
+    for (double v : cfg.snr_db) snrs.push_back(jnum(v));
+    for (const PointStats& r : rows)
+        results.push_back(jobj({{"decoder", jstr(to_string(r.decoder))},
+                                {"snr_db", jnum(r.snr_db)},
+                                {"frames", jint(r.frames)},
+                                {"bit_errors", jint(r.bit_errors)},
+                                {"frame_errors", jint(r.frame_errors)},
+                                {"ber", jnum(r.ber)},
+                                {"fer", jnum(r.fer)},
+                                {"fer_ci95", jnum(r.fer_ci95)},
+                                {"avg_iters", jnum(r.avg_iters)},
+                                {"iters_ci95", jnum(r.iters_ci95)},
+                                {"avg_pe_activations", jnum(r.avg_pe_activations)},
+                                {"norm_computations", jnum(r.norm_computations)},
+                                {"low_confidence", jbool(r.low_confidence)}}));
+    const Json j = jobj({{"config", jobj({{"n", jint(cfg.code.n)},
+                                          {"k", jint(cfg.code.k)},
+                                          {"frozen", jarr(frozen)},
+                                          {"code_source", jstr(cfg.code_source)},
+                                          {"decoders", jarr(decoders)},
+                                          {"snr_db", jarr(snrs)},
+                                          {"alpha", jnum(cfg.alpha)},
+                                          {"max_iter", jint(cfg.max_iter)},
+                                          {"min_frame_errors", jint(cfg.min_frame_errors)},
+                                          {"max_frames", jint(cfg.max_frames)},
+                                          {"seed", jint(cfg.seed)},
+                                          {"workers", jint(cfg.workers)},
+                                          {"noiseless", jbool(cfg.noiseless)}})},
+                         {"results", jarr(results)}});
+    std::string o;
+    dump2(j, 0, o);
+    return o + "\n";
 }
 
 std::vector<SavingsRow> compute_savings(std::span<const PointStats> rows) {

@@ -85,18 +85,23 @@ std::optional<CsfgDecision> check_csfg(const MessageState& state, const PolarCod
 Bits mld_oracle(std::span<const double> r_block, std::span<const std::uint8_t> frozen_block,
                 long long max_candidates) {
     if (r_block.size() != frozen_block.size()) throw std::invalid_argument("mld_oracle: span length mismatch");
+    if (!is_power_of_two(static_cast<int>(r_block.size())))
+        throw std::invalid_argument("mld_oracle: length must be a power of two");
     std::vector<int> free_rows;
     for (size_t i = 0; i < frozen_block.size(); ++i)
         if (!frozen_block[i]) free_rows.push_back(static_cast<int>(i));
     if (free_rows.size() >= 62 || (1ll << free_rows.size()) > max_candidates)
-        throw std::invalid_argument("mld_oracle: too many candidates");
+        throw std::invalid_argument("mld_oracle: candidate budget exceeded");
     const long long count = 1ll << free_rows.size();
     Bits best;
     double best_score = 0.0;
     Bits u(r_block.size(), 0);
     for (long long c = 0; c < count; ++c) {
         std::fill(u.begin(), u.end(), 0);
-        for (size_t b = 0; b < free_rows.size(); ++b) u[free_rows[b]] = (c >> b) & 1;
+        // counter bits MSB-first onto the free rows in index order: candidates in
+        // lexicographic u order, strict improvements keep the smallest maximizer
+        const size_t nf = free_rows.size();
+        for (size_t b = 0; b < nf; ++b) u[free_rows[b]] = (c >> (nf - 1 - b)) & 1;
         const Bits x = polar_transform(u);
         double score = 0.0;
         for (size_t i = 0; i < x.size(); ++i) score += x[i] ? -r_block[i] : r_block[i];

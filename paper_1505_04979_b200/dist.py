@@ -47,15 +47,22 @@ def simulate_sweep_sharded(code, decoder, seed: int, frames_per_point: int, snrs
     """run_sweep's counters with fixed frame counts (min_frame_errors = inf), sharded.
 
     point_fn(code, decoder, seed, first, count, ebn0, alpha, max_iter) -> counters dict;
-    defaults to the GPU path (paper_1505_04979_b200.simulate_point on this rank's device).
+    defaults to the GPU path (paper_1505_04979_b200.simulate_point on a Context of this
+    rank's device: `device`, else LOCAL_RANK).
     Trial indices restart at 0 for every Eb/N0 point, as in run_point
     (src/sim_harness.cpp:141-147), so every point is sharded the same way.
     """
     if point_fn is None:
+        import os
+
         import paper_1505_04979_b200 as P
+        # this rank's GPU: the `device` argument, else torchrun's LOCAL_RANK
+        dev = device if device is not None else int(os.environ.get("LOCAL_RANK", "0"))
+        dev = dev.index if hasattr(dev, "index") and dev.index is not None else int(dev)
+        pctx = P.Context(dev)
 
         def point_fn(code, decoder, seed, first, count, ebn0, alpha, max_iter):
-            return P.simulate_point(code, decoder, seed, first, count, ebn0, alpha, max_iter)
+            return P.simulate_point(code, decoder, seed, first, count, ebn0, alpha, max_iter, ctx=pctx)
     first, count = shard_range(frames_per_point, rank, world)
     local = [point_fn(code, decoder, seed, first, count, snr, alpha, max_iter) for snr in snrs]
     return allreduce_counters(local, group=group, device=device)

@@ -183,6 +183,22 @@ static void host_cases() {
         CHECK(count_active(f2) == 11 && !is_pe_active(f2, 2, 0) && is_pe_active(f2, 1, 0));
         CHECK(mld_oracle(std::vector<double>{3.0, 1.0, 2.0, 4.0}, Bits{1, 1, 1, 0}) == Bits(4, 0));
         CHECK(throws([] { mld_oracle(std::vector<double>(16, 1.0), Bits(16, 0), 8); }));
+        // csfg_freeze.cpp:44-53: texts, power-of-two length, MSB-first enumeration (ties keep
+        // the lexicographically smallest u: all-zero LLRs tie every candidate)
+        auto what = [](auto f) {
+            try {
+                f();
+            } catch (const std::invalid_argument& e) {
+                return std::string(e.what());
+            }
+            return std::string();
+        };
+        CHECK(what([] { mld_oracle(std::vector<double>(16, 1.0), Bits(16, 0), 8); }) ==
+              "mld_oracle: candidate budget exceeded");
+        CHECK(what([] { mld_oracle(std::vector<double>(3, 1.0), Bits(3, 1)); }) ==
+              "mld_oracle: length must be a power of two");
+        CHECK(what([] { mld_oracle(std::vector<double>(4, 1.0), Bits(2, 1)); }) == "mld_oracle: span length mismatch");
+        CHECK(mld_oracle(std::vector<double>(4, 0.0), Bits{1, 0, 0, 1}) == Bits(4, 0));
         // freeze_decision accepts exactly when it equals the block ML decision
         std::mt19937_64 gen(9002);
         std::uniform_real_distribution<double> uni(-5.0, 5.0);
@@ -236,6 +252,46 @@ static void host_cases() {
     CHECK(back.size() == 3 && back[2].avg_iters == 20.0);
     const auto sv = compute_savings(rows);
     CHECK(sv.size() == 1 && std::fabs(sv[0].iters_vs_baseline - 0.5) < 1e-12);
+}
+
+// results_json in nlohmann::json::dump(2) form (sim_harness.cpp:250-289): sorted keys,
+// one element per line, shortest round-trip doubles laid out like nlohmann's dtoa
+static void json_case() {
+    SimConfig cfg;
+    cfg.code = PolarCode::construct(4, 2, 0.5);
+    cfg.code_source = "construct \"z\"";
+    cfg.decoders = {DecoderKind::csfg};
+    cfg.snr_db = {1.5, 0.0001, 1e16, 1e15};  // 1e15: 16 integer digits > 15 -> e-notation
+    cfg.seed = 18446744073709551615ull;
+    PointStats r;
+    r.decoder = DecoderKind::csfg;
+    r.snr_db = 1.5;
+    r.frames = 256;
+    r.bit_errors = 3;
+    r.frame_errors = 1;
+    r.ber = 3.0 / 512.0;
+    r.fer = 1.0 / 256.0;
+    r.fer_ci95 = 1e-05;
+    r.avg_iters = 40.0;
+    r.iters_ci95 = 0.0;
+    r.avg_pe_activations = 1234567.0;
+    r.norm_computations = 0.1;
+    r.low_confidence = true;
+    const std::vector<PointStats> rows{r};
+    const std::string want =
+        "{\n  \"config\": {\n    \"alpha\": 0.9375,\n    \"code_source\": \"construct \\\"z\\\"\",\n"
+        "    \"decoders\": [\n      \"csfg\"\n    ],\n    \"frozen\": [\n      1,\n      2\n    ],\n"
+        "    \"k\": 2,\n    \"max_frames\": 100000,\n    \"max_iter\": 40,\n    \"min_frame_errors\": 100,\n"
+        "    \"n\": 4,\n    \"noiseless\": false,\n    \"seed\": 18446744073709551615,\n"
+        "    \"snr_db\": [\n      1.5,\n      0.0001,\n      1e+16,\n      1e+15\n    ],\n"
+        "    \"workers\": 1\n  },\n  \"results\": [\n    {\n      \"avg_iters\": 40.0,\n"
+        "      \"avg_pe_activations\": 1234567.0,\n      \"ber\": 0.005859375,\n      \"bit_errors\": 3,\n"
+        "      \"decoder\": \"csfg\",\n      \"fer\": 0.00390625,\n      \"fer_ci95\": 1e-05,\n"
+        "      \"frame_errors\": 1,\n      \"frames\": 256,\n      \"iters_ci95\": 0.0,\n"
+        "      \"low_confidence\": true,\n      \"norm_computations\": 0.1,\n      \"snr_db\": 1.5\n    }\n  ]\n}\n";
+    const std::string got = results_json(cfg, rows);
+    CHECK(got == want);
+    if (got != want) std::printf("%s", got.c_str());
 }
 
 static void gpu_cases() {
@@ -423,11 +479,26 @@ static void gpu_cases() {
     s2.max_frames = 5000;
     const auto r2 = run_sweep(s2);
     CHECK(r2[0].frames == 256 && r2[0].frame_errors >= 3);
+    // proj/test_output.txt:16-18 (acceptance.cpp:129-150): 3.0 dB, seed 61803, device batch
+    // counters merged with the stop rule -> 7168 frames, FER 0.01465 / 0.01409 / 0.01423
+    SimConfig a3;
+    a3.code = PolarCode::construct(1024, 512, 0.5);
+    a3.snr_db = {3.0};
+    a3.seed = 61803;
+    const auto r3 = run_sweep(a3);
+    char buf[3][96];
+    for (int d = 0; d < 3; ++d)
+        std::snprintf(buf[d], sizeof(buf[d]), "%lld %.4g %.2f %.0f", r3[d].frames, r3[d].fer, r3[d].avg_iters,
+                      r3[d].avg_pe_activations);
+    CHECK(std::string(buf[0]) == "7168 0.01465 40.00 204800");
+    CHECK(std::string(buf[1]) == "7168 0.01409 24.70 126442");
+    CHECK(std::string(buf[2]) == "7168 0.01423 24.69 123124");
 }
 
 int main(int argc, char** argv) {
     const bool cpu_only = argc > 1 && std::strcmp(argv[1], "--cpu-only") == 0;
     host_cases();
+    json_case();
     if (!cpu_only) gpu_cases();
     std::printf("%d passed, %d failed\n", g_pass, g_fail);
     return g_fail;

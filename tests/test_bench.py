@@ -39,3 +39,33 @@ def test_our_arm_line():
     assert r["bound"] == "alu" and 0 < r["frac"] < 1 and r["peak"] > 0
     assert "sm_mhz" in d["clocks"] and isinstance(d["clocks"]["reasons"], list)
     assert d["config"]["frames_per_step"] == 7 * 4000
+
+
+def test_gpus_n_relaunches_one_rank_per_gpu():
+    """`bench.py --gpus N` outside torchrun starts N ranks (torch.distributed.run on
+    127.0.0.1); the reference arm then runs on rank 0 only and prints one line."""
+    sys.path.insert(0, ROOT)
+    import bench
+    cmd = bench.launch_command(["--gpus", "4", "--steps", "2"], 4, 29555)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29555" in cmd
+    assert cmd[-3:] == ["--gpus", "4", "--steps", "2"][-3:]
+    d = _line(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1"], timeout=900)
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+@pytest.mark.gpu
+def test_our_arm_under_torchrun_uses_nccl():
+    """One rank launched by torchrun takes the multi-GPU path: NCCL process group, the
+    counters all-reduce and the max-over-ranks timing."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr=127.0.0.1", "--master-port=29517", os.path.join(ROOT, "bench.py"), "--gpus", "1",
+           "--steps", "1", "--warmup", "3", "--frames", "2000", "--no-cpu-baseline", "--no-e2e"]
+    env = dict(os.environ, NCCL_DEBUG="INFO")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    d = json.loads(lines[-1])
+    assert d["n_gpus"] == 1 and d["config"]["frames_per_step"] == 7 * 2000
+    assert "NCCL" in r.stdout + r.stderr
+    assert d["gen_decode"]["counters_equal_decode_only"]
