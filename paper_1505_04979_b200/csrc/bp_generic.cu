@@ -272,6 +272,10 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
             }
 
             if (a.kind == 0) continue;
+            if (m == 0) {  // no stage ran: L(0) = L(m) (bp_core.cpp:53), x_hat = R(0) + L(0) < 0
+                if (tid == 0) xh[0] = O::add(R0(0), a.frozen_rows[0] ? cap : T(0)) < T(0) ? 1u : 0u;
+                __syncthreads();
+            }
             const int pin = csfg ? s_frontier : 0;
             if (csfg && pin >= n) continue;
             // ---- gmatrix_converged (src/bp_core.cpp:95-102), pinned prefix
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(BLOCK) bp_generic_kernel(DecodeArgs a) {
                 bool ub = false;
                 if (i < n)
                     ub = (i < pin) ? ((dec_u[i >> 5] >> (i & 31)) & 1u)
-                                   : (!a.frozen_rows[i] && R[i] < T(0));
+                                   : (!a.frozen_rows[i] && (m == 0 ? R0(i) : R[i]) < T(0));  // m = 0: R(m) = R(0)
                 const uint32_t wu = __ballot_sync(0xffffffffu, ub);
                 if (lane == 0) {
                     wb0[i >> 5] = wu;
