@@ -31,6 +31,9 @@ _f64p = C_.POINTER(C_.c_double)
 _u64p = C_.POINTER(C_.c_uint64)
 
 KIND = {"baseline": 0, "gmatrix": 1, "csfg": 2}
+# decode/decode_batch use this library when none is passed (None: the C restatement);
+# tests/conftest.py points it at the compiled reference (REF) for the GPU parity tests
+DEFAULT_LIB = None
 STOP_NAMES = ("max_iter", "gmatrix_converged", "csfg_complete")
 
 
@@ -129,7 +132,7 @@ def trials(seed, first, count, frozen, ebn0, noiseless=False, threads=None, lib=
 
 def decode(kind, frozen, llr, alpha=0.9375, max_iter=40, prec=32, lib=None, ev_cap=4096):
     """One frame through the oracle. Returns dict(u_hat, iterations, pe, stop, n_events, events)."""
-    lib = lib or C
+    lib = lib or DEFAULT_LIB or C
     n = frozen.size
     if prec == 32:
         llr = np.ascontiguousarray(llr, np.float32)
@@ -159,7 +162,7 @@ def decode_batch(kind, frozen, llr, alpha=0.9375, max_iter=40, prec=32, lib=None
     want_events=False passes no event counter, so csfg records no FreezeEvent
     list (the reference's decode_trial does that only with --trace,
     sim_harness.cpp:84-90); "n_events" is then None."""
-    lib = lib or C
+    lib = lib or DEFAULT_LIB or C
     llr = np.ascontiguousarray(llr, np.float32 if prec == 32 else np.float64)
     frames, n = llr.shape
     if lib is C:

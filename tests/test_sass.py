@@ -35,8 +35,9 @@ def _functions(sass):
 @pytest.mark.skipif(not os.path.exists(CUOBJDUMP), reason="cuobjdump absent")
 def test_decoder_kernels_have_no_fused_multiply_add():
     fns = _functions(_sass())
-    dec = {k: v for k, v in fns.items() if "bp_warp_kernel" in k or "bp_generic_kernel" in k}
-    assert len(dec) >= 13
+    dec = {k: v for k, v in fns.items()
+           if "bp_warp_kernel" in k or "bp_generic_kernel" in k or "bp_cta_kernel" in k}
+    assert len(dec) >= 13 and any("bp_cta_kernel" in k for k in dec)
     for name, lines in dec.items():
         for ln in lines:
             m = re.search(r"\bFFMA2?\b[^;]*;", ln)
