@@ -209,6 +209,7 @@ struct Dec {
     Smem* sm;
     float4* r0g;  // this warp's channel LLRs in global scratch, lane-private pass-0 layout (n < 1024)
     uint32_t tb;  // this warp's TMEM columns (n = 1024)
+    const uint32_t* fzt;  // n = 1024: walk0's frozen-row field words, [F/32][lane] (shared by the CTA)
     const DecodeArgs* a;
     int lane;
     float alpha;
@@ -271,6 +272,7 @@ struct Dec {
     __device__ __forceinline__ void load_L(float (&Lt)[P]) {
         constexpr int q = PL::pass_of(T - 1);
         if constexpr (T == M && TM) {
+            tm::wait_st();  // a stage m-1 commit's column update (apply_tm)
             tm::ld_row<kTG>(tb + PL::C_LM, Lt);
             tm::wait_ld();
         } else if constexpr (T == M && KIND == 2) {
@@ -649,7 +651,6 @@ struct Dec {
         s_last_ = M - 1;
         done_ = false;
         uint32_t skip = 0u;  // stages already past (one decision per stage)
-        const uint32_t fz0 = FZ[0];
 #pragma unroll 1
         while (true) {
             const int jf = frontier >> 5;
@@ -692,9 +693,7 @@ struct Dec {
                 const uint32_t o = __shfl_xor_sync(kFull, u, 1 << gp);
                 if (!((lane >> gp) & 1)) u ^= o;
             }
-            const uint32_t fzw = ((fz0 >> j00) & 0xFFFFu) | (((fz0 >> j01) & 0xFFu) << 16) |
-                                 (((fz0 >> j02) & 0xFu) << 24) | (((fz0 >> j03) & 3u) << 28) |
-                                 (((fz0 >> j04) & 1u) << 30);
+            const uint32_t fzw = fzt[jf * 32 + lane];  // frozen rows of the five blocks, same fields
             const uint32_t V = __reduce_or_sync(kFull, u & fzw);
             uint32_t acc = (uint32_t)((V & 0xFFFFu) == 0u) | ((uint32_t)(((V >> 16) & 0xFFu) == 0u) << 1) |
                            ((uint32_t)(((V >> 24) & 0xFu) == 0u) << 2) | ((uint32_t)(((V >> 28) & 3u) == 0u) << 3) |
@@ -855,28 +854,29 @@ struct Dec {
 #pragma unroll
         for (int tp = 0; tp < 4; ++tp)
             if (tp < g) viol |= viol >> (1 << tp);
-        int F = frontier, slast = s_last_, Al = 0;
+        // the scan on window offsets (f = frontier - A5 < 16); rows from offset lim
+        // on do not exist, and a commit reaching them completes the frame
+        uint32_t vt[5];
+#pragma unroll
+        for (int t = 0; t < 5; ++t) vt[t] = __shfl_sync(kFull, viol, t);  // off the scan's chain
+        const int lim = N - A5;
+        int f = frontier - A5, Al = 0;
         uint32_t cm = 0u;
-        bool done = false;
 #pragma unroll
         for (int t = 0; t < 5; ++t) {
-            const uint32_t vt = __shfl_sync(kFull, viol, t);
             const int B = 16 >> t;
-            const int A = F & ~(B - 1);
-            w.At[t] = A;
-            Al = lane == t ? A : Al;
-            const bool acc = !done && !((vt >> (A - A5)) & 1u);
+            const int o = f & ~(B - 1);
+            w.At[t] = A5 + o;
+            Al = lane == t ? o : Al;
+            const bool acc = f < lim && !((vt[t] >> o) & 1u);
             cm |= (uint32_t)acc << t;
-            F = acc ? A + B : F;
-            const bool fin = acc && F >= N;
-            slast = fin ? 5 + t : slast;
-            done = done || fin;
+            f = acc ? o + B : f;
         }
-        w.Al = Al;
+        w.Al = A5 + Al;
         w.cm = cm;
-        s_last_ = slast;
-        frontier = F;
-        done_ = done;
+        done_ = f >= lim;
+        if (done_) s_last_ = 5 + (31 - __clz(cm));  // the commit that reached n is the iteration's last
+        frontier = A5 + f;
     }
 
     // apply_freeze (csfg_freeze.cpp:82-93) for the last-pass commits of one
@@ -974,13 +974,17 @@ struct Dec {
     // pinned G-check).
     __device__ __forceinline__ bool finish_iter() {
         if constexpr (TM) {
+            PBP_T0(tw);
             LateTM w;
             walk_tm(w);
+            PBP_T1(tw, 3);
+            PBP_T0(ta);
             int dinact = 0;
             if (nce_) dinact = apply_commits(w);
             if (w.cm) apply_tm(w, dinact);
             if (lane < M) inact += dinact;
             __syncwarp();
+            PBP_T1(ta, 4);
         } else {
             PBP_T0(tw);
             LastWalk w;
@@ -1192,8 +1196,7 @@ struct Dec {
                 tm::ld1(tb + PL::C_LM + j, &v);
                 tm::wait_ld();
                 if (lane == r9 / P) v = xb ? -kCap : kCap;
-                tm::st1(tb + PL::C_LM + j, v);
-                tm::wait_st();
+                tm::st1(tb + PL::C_LM + j, v);  // completed before the next L(m) load (wait_st there)
             }
         }
         // 2. decided_u (:87), protection masks, event log (:91-92): lane t
@@ -1300,7 +1303,7 @@ struct Dec {
                 resaturate<PL::pass_of(S + 1)>();
             else
                 __syncwarp();  // X holds other lanes' L(e) writes of the previous iteration
-            PBP_T1(tr, 2);
+            PBP_T1(tr, 0);
         }
         PBP_T0(tm);
         float Lt[P];
@@ -1314,7 +1317,13 @@ struct Dec {
             PBP_T0(ts);
             if constexpr (S < PL::SL && TM) {
                 tm::st_row<kTG>(tb + PL::C_S + 32u * S, R);  // R(S+1), pass-0 layout
-                if constexpr (S == PL::SL - 1) walk0();
+                if constexpr (S == PL::SL - 1) {
+                    PBP_T1(ts, 1);
+                    PBP_T0(tw0);
+                    walk0();
+                    PBP_T1(tw0, 2);
+                    return true;
+                }
             } else if constexpr (S < PL::SL) {
                 snapshot<S>();
                 if constexpr (S == PL::SL - 1) walk_early();
@@ -1641,6 +1650,10 @@ struct Dec {
 template <int M>
 constexpr int kMinWarps = M >= 10 ? 1 : (M == 9 ? 12 : 20);
 
+// CTA-shared shared memory after the warps' own: walk0's frozen-field table (n = 1024 csfg)
+template <int M, int KIND>
+constexpr size_t extra_smem() { return (Plan<M>::TM && KIND == 2) ? 32 * 32 * sizeof(uint32_t) : 0; }
+
 // n = 1024: eight warps (frames) per CTA, one CTA per SM, so the CTA's TMEM
 // allocation (all 512 columns) gives each warp 256 columns of its lane quarter
 template <int M, int KIND, bool XH = false>
@@ -1652,10 +1665,24 @@ __global__ void __launch_bounds__(32 * Plan<M>::WARPS, Plan<M>::TM ? 1 : kMinWar
         __shared__ uint32_t tbase;
         const int warp = threadIdx.x >> 5;
         if (warp == 0) tm::alloc512(&tbase);
+        if constexpr (KIND == 2) {
+            // walk0's frozen-row fields for every frontier word jf (pass-0 layout, bit j of
+            // fz0 = row lane + 32 j): blocks of 16, 8, 4, 2, 1 words at offsets 0, 16, 24, 28, 30
+            uint32_t* t = reinterpret_cast<uint32_t*>(reinterpret_cast<typename D::Smem*>(wsm) + Plan<M>::WARPS);
+            for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
+                const int jf = i >> 5, ln = i & 31;
+                uint32_t fz0 = 0u;
+                for (int j = 0; j < 32; ++j) fz0 |= (uint32_t)(a.frozen_rows[ln + 32 * j] != 0) << j;
+                t[i] = ((fz0 >> (jf & ~15)) & 0xFFFFu) | (((fz0 >> (jf & ~7)) & 0xFFu) << 16) |
+                       (((fz0 >> (jf & ~3)) & 0xFu) << 24) | (((fz0 >> (jf & ~1)) & 3u) << 28) |
+                       (((fz0 >> jf) & 1u) << 30);
+            }
+        }
         tm::fence_before();
         __syncthreads();
         tm::fence_after();
         dec.tb = tm::warp_base(tbase, warp);
+        dec.fzt = reinterpret_cast<const uint32_t*>(reinterpret_cast<typename D::Smem*>(wsm) + Plan<M>::WARPS);
         dec.run(a, reinterpret_cast<typename D::Smem*>(wsm) + warp, threadIdx.x & 31);
         tm::fence_before();
         __syncthreads();
@@ -1686,7 +1713,7 @@ size_t warp_smem_bytes(int m, int kind) {
 template <int M, int KIND, bool XH>
 static cudaError_t launch_wx(const DecodeArgs& a, int grid, cudaStream_t st) {
     constexpr int W = wk::Plan<M>::WARPS;
-    const size_t smem = W * sizeof(typename wk::Dec<M, KIND, XH>::Smem);
+    const size_t smem = W * sizeof(typename wk::Dec<M, KIND, XH>::Smem) + wk::extra_smem<M, KIND>();
     cudaError_t e = cudaFuncSetAttribute(wk::bp_warp_kernel<M, KIND, XH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1725,7 +1752,7 @@ template <int M, int KIND>
 static int occ_w() {
     int nb = 0;
     constexpr int W = wk::Plan<M>::WARPS;
-    const size_t smem = W * sizeof(typename wk::Dec<M, KIND>::Smem);
+    const size_t smem = W * sizeof(typename wk::Dec<M, KIND>::Smem) + wk::extra_smem<M, KIND>();
     cudaFuncSetAttribute(wk::bp_warp_kernel<M, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wk::bp_warp_kernel<M, KIND>, 32 * W, smem) != cudaSuccess)
         return 0;

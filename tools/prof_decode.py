@@ -52,7 +52,7 @@ if hasattr(P.lib, "pbp_prof_read") and os.environ.get("PBP_LIB"):
                                            P._abi.i64p(cnt.data_ptr()), None))
     ctx.synchronize()
     P.lib.pbp_prof_read(buf, 1)
-    names = ["stage math", "snapshot", "resat/sync", "walk", "commits", "gcheck", "frame load", "iter loop"]
+    names = ["stage math", "snapshot", "walk0/resat", "walk", "commits", "gcheck", "frame load", "iter loop"]
     tot = buf[7] + buf[6]
     its = cnt.cpu().tolist()[3]
     for i, nm in enumerate(names):
