@@ -187,6 +187,9 @@ extern "C" int pbp_prof_read(unsigned long long* out, int reset) {
     }
     return 0;
 }
+#ifndef PBP_SLOT_APPLY_TM
+#define PBP_SLOT_APPLY_TM 4
+#endif
 #define PBP_T0(v) const long long v = clock64()
 #define PBP_T1(v, k) do { if (lane == 0) prof[k] += clock64() - (v); } while (0)
 #else
@@ -879,6 +882,107 @@ struct Dec {
         frontier = A5 + f;
     }
 
+    // apply_freeze (csfg_freeze.cpp:82-93) for the first-pass commits of one
+    // iteration (TM, rare: ~1 per frame at 3 dB), kept compact so that it costs
+    // little instruction cache when it runs. Commit k (stage S <= 4) covers the
+    // 16 >> S registers j0.. of every lane (pass-0 layout, row = lane + 32 j).
+    // Returns this lane's newly inactive top rows (lane = a later stage).
+    __device__ __forceinline__ int apply_early_tm() {
+        static_assert(M == 10 && PL::SL == 5, "apply_early_tm: n = 1024 layout");
+        const int nce = nce_, fr_start = fr_start_;
+        __syncwarp();
+        int dinact = 0;
+#pragma unroll 1
+        for (int k = 0; k < nce; ++k) {
+            const int S = sm->cS[k], bi = sm->cbi[k];
+            const int g = M - 1 - S, W = 16 >> S;
+            const int start = bi << g, sz = 1 << g;
+            const int j0 = (start >> 5) & 31;
+            const uint32_t wm = (W >= 32) ? 0xffffffffu : ((1u << W) - 1u);
+            // u_hat of the block (walk0); x_hat = T(u_hat): the transform is an involution
+            const uint32_t uu = sm->su[k][lane];
+            uint32_t xx = uu;
+#pragma unroll 1
+            for (int tp = 0; tp < 4 - S; ++tp) xx ^= (xx >> (1 << tp)) & c_jmask[tp];
+#pragma unroll
+            for (int gp = 0; gp < 5; ++gp) {
+                const uint32_t o = __shfl_xor_sync(kFull, xx, 1 << gp);
+                if (!((lane >> gp) & 1)) xx ^= o;
+            }
+            const uint32_t xbits = (xx >> j0) & wm, ubits = (uu >> j0) & wm;
+            // 1. saturate L(S+1) (csfg_freeze.cpp:84-86): register level, or the
+            //    pass boundary L(5) (re-saturated before each of its reads)
+            if (S < 4) {
+                sm->pm[S][lane] |= wm << j0;
+                sm->ss[S][lane] = (sm->ss[S][lane] & ~(wm << j0)) | (xbits << j0);
+                prot |= 1u << S;
+            } else {
+                if (lane == 0) sm->xprot[0][bi >> 5] |= 1u << (bi & 31);
+                const uint32_t xw = __ballot_sync(kFull, xbits & 1u);  // one register: row word j0
+                if (lane == 0) sm->sat[start >> 5] = xw;
+            }
+            // 2. decided_u (:87): row-order word j0 + i collects bit i of every lane
+            uint32_t dw = 0u;
+#pragma unroll 1
+            for (int i = 0; i < W; ++i) {
+                const uint32_t b = __ballot_sync(kFull, (ubits >> i) & 1u);
+                dw = lane == i ? b : dw;
+            }
+            if (lane < W) sm->dec_u[(start >> 5) + lane] = dw;
+            // 3. inactive top rows of the stages after S; only the first commit can
+            //    re-cover rows decided before (freeze_stage still holds their stages):
+            //    those already inactive at s2 are counted once (packed warp sums)
+            if (lane > S && lane < M) dinact += sz >> 1;
+            if (k == 0 && start < fr_start) {
+                uint32_t c[5] = {0u, 0u, 0u, 0u, 0u};  // stages (1,2) .. (9): 16-bit fields
+#pragma unroll 1
+                for (int r = start + lane; r < fr_start; r += 32) {
+                    const int fo = sm->fst[r];
+                    const int lo = fo > S ? fo : S;
+                    const uint32_t top = __brev(~(uint32_t)r) >> (32 - M);  // bit s2: top row at s2
+                    const uint32_t msk = top & ~((2u << lo) - 1u);
+#pragma unroll
+                    for (int q = 0; q < 5; ++q)
+                        c[q] += ((msk >> (2 * q + 1)) & 1u) | (((msk >> (2 * q + 2)) & 1u) << 16);
+                }
+#pragma unroll
+                for (int q = 0; q < 5; ++q) {
+                    const uint32_t t = __reduce_add_sync(kFull, c[q]);
+                    if (lane == 2 * q + 1) dinact -= (int)(t & 0xffffu);
+                    if (lane == 2 * q + 2 && lane < M) dinact -= (int)(t >> 16);
+                }
+            }
+            //    freeze_stage over the block (:86), 16 bytes per lane and step
+            {
+                const uint32_t w4 = 0x01010101u * (uint32_t)S;
+#pragma unroll 1
+                for (int i = 16 * lane; i < sz; i += 512)
+                    *reinterpret_cast<uint4*>(&sm->fst[start + i]) = make_uint4(w4, w4, w4, w4);
+            }
+            // 4. event log (:91-92)
+            if (lane == 0 && a->events && nev < a->ev_cap) {
+                int* e = a->events + ((long long)frame_ * a->ev_cap + nev) * 5;
+                e[0] = it;
+                e[1] = S;
+                e[2] = bi;
+                e[3] = start;
+                e[4] = sz;
+            }
+            if (XH && a->ev_xhat && nev < a->ev_cap) {  // FreezeEvent::x_hat (trace calls only)
+                uint32_t xw = 0u;
+#pragma unroll 1
+                for (int i = 0; i < W; ++i) {
+                    const uint32_t b = __ballot_sync(kFull, (xbits >> i) & 1u);
+                    xw = lane == i ? b : xw;
+                }
+                if (lane < W) a->ev_xhat[((long long)frame_ * a->ev_cap + nev) * NW + (start >> 5) + lane] = xw;
+            }
+            ++nev;
+            __syncwarp();
+        }
+        return dinact;
+    }
+
     // apply_freeze (csfg_freeze.cpp:82-93) for the last-pass commits of one
     // iteration (TM): lane i takes window row A5 + i (saturation of L(S+1),
     // freeze_stage, decided_u by ballot), lane t takes stage 5 + t's commit
@@ -980,11 +1084,13 @@ struct Dec {
             PBP_T1(tw, 3);
             PBP_T0(ta);
             int dinact = 0;
-            if (nce_) dinact = apply_commits(w);
+            if (nce_) dinact = apply_early_tm();
+            PBP_T1(ta, 4);
+            PBP_T0(tb2);
             if (w.cm) apply_tm(w, dinact);
             if (lane < M) inact += dinact;
             __syncwarp();
-            PBP_T1(ta, 4);
+            PBP_T1(tb2, PBP_SLOT_APPLY_TM);
         } else {
             PBP_T0(tw);
             LastWalk w;
