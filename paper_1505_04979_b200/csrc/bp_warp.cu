@@ -992,6 +992,10 @@ struct Dec {
     __device__ __forceinline__ void apply_tm(const LateTM& w, int& dinact) {
         const uint32_t cm = w.cm;
         const int A5 = w.A5, r = A5 + lane;
+        // stage m-1 commit: its L(m) column, loaded first (the rest hides the latency)
+        const bool c9 = (cm >> 4) & 1u;
+        float v9 = 0.f;
+        if (c9) tm::ld1(tb + PL::C_LM + (w.At[4] & 31), &v9);
         int Sr = -1;
         uint32_t xb = 0u;
         int tr = 0;
@@ -1030,31 +1034,30 @@ struct Dec {
             }
             sm->fst[r] = (uint8_t)Sr;
         }
-        if ((cm >> 4) & 1u) {  // stage m-1: L(m) of one row, TMEM column j of lane owner
+        if (c9) {  // stage m-1: L(m) of one row, TMEM column j of lane owner
             const int r9 = w.At[4];
             const uint32_t x9 = (w.x[4] >> (r9 - A5)) & 1u;
-            const int j = r9 & 31;
-            float v;
-            tm::ld1(tb + PL::C_LM + j, &v);
             tm::wait_ld();
-            if (lane == (r9 >> 5)) v = x9 ? -kCap : kCap;
-            tm::st1(tb + PL::C_LM + j, v);
-            tm::wait_st();
+            if (lane == (r9 >> 5)) v9 = x9 ? -kCap : kCap;
+            tm::st1(tb + PL::C_LM + (r9 & 31), v9);  // completed before the next L(m) load (wait_st there)
         }
-        // decided_u over the window (two row-order words)
+        // decided_u over the window (two row-order words; shared atomics: no round trip)
         const uint32_t cvw = __ballot_sync(kFull, cov), uw = __ballot_sync(kFull, cov && ub);
         if (lane < 2) {
             const int wd = (A5 >> 5) + lane, sh = A5 & 31;
             const uint32_t mk = lane == 0 ? cvw << sh : (sh ? cvw >> (32 - sh) : 0u);
             const uint32_t vv = lane == 0 ? uw << sh : (sh ? uw >> (32 - sh) : 0u);
-            if (mk) sm->dec_u[wd] = (sm->dec_u[wd] & ~mk) | vv;
+            if (mk) {
+                atomicAnd(&sm->dec_u[wd], ~mk);
+                atomicOr(&sm->dec_u[wd], vv);
+            }
         }
         // inactive top rows: a stage-S block of B rows has B/2 top rows at every later stage
         if (lane < M) dinact += (int)((__brev((cm << 5) & ((1u << lane) - 1u)) >> (32 - M)) >> 1);
         if ((cm >> lane) & 1u) {
             const int S = 5 + lane, B = 16 >> lane, A = w.Al;
             const uint32_t wm = (1u << B) - 1u;
-            if (lane < 4) sm->pm[PL::NLR + lane][A >> 5] |= wm << (A & 31);  // L(S+1) in shared slot S - 5
+            if (lane < 4) atomicOr(&sm->pm[PL::NLR + lane][A >> 5], wm << (A & 31));  // L(S+1): shared slot S - 5
             const int e_ix = nev + __popc(cm & ((1u << lane) - 1u));
             if (a->events && e_ix < a->ev_cap) {
                 int* e = a->events + ((long long)frame_ * a->ev_cap + e_ix) * 5;
@@ -1291,19 +1294,6 @@ struct Dec {
                 base[((j >> 2) * 32 + owner) * 4 + (j & 3)] = xbit ? -kCap : kCap;
             }
             sm->fst[r] = (uint8_t)Sr;
-        }
-        if constexpr (TM) {
-            // L(m) of the stage m-1 block (one row) in TMEM: column j of lane owner
-            if ((cmask >> (NL - 1)) & 1u) {
-                const int r9 = __shfl_sync(kFull, w.Al, NL - 1);
-                const uint32_t xb = (w.x[NL - 1] >> (r9 - w.A5)) & 1u;
-                const int j = r9 % P;
-                float v;
-                tm::ld1(tb + PL::C_LM + j, &v);
-                tm::wait_ld();
-                if (lane == r9 / P) v = xb ? -kCap : kCap;
-                tm::st1(tb + PL::C_LM + j, v);  // completed before the next L(m) load (wait_st there)
-            }
         }
         // 2. decided_u (:87), protection masks, event log (:91-92): lane t
         uint32_t myprot = 0u;
