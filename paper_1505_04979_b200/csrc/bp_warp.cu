@@ -297,7 +297,8 @@ struct Dec {
             constexpr int sl = PL::reg_slot(T);
 #pragma unroll
             for (int j = 0; j < P; ++j) Lt[j] = Lr[sl][j];
-            if (prot & (1u << sl)) {  // uniform, rare: boundary rows read as +-CAP
+            // TM: fixed up once after each sweep (fixup_regs), off the stages' code path
+            if (!TM && (prot & (1u << sl))) {  // uniform, rare: boundary rows read as +-CAP
                 const uint32_t pm = sm->pm[sl][lane], ss = sm->ss[sl][lane];
 #pragma unroll
                 for (int j = 0; j < P; ++j)
@@ -330,7 +331,7 @@ struct Dec {
             constexpr int sl = PL::smem_slot(S);
             constexpr int ps = PL::prot_slot(S);
             constexpr int d = 1 << (M - 1 - S);  // last pass: b = 0
-            if (!(prot & (1u << ps))) {
+            if (!TM && !(prot & (1u << ps))) {  // TM: one (predicated) version, smaller hot code
 #pragma unroll
                 for (int c = 0; c < P / 4; ++c)
                     sm->Ls[sl][c][lane] = make_float4(Lt[4 * c], Lt[4 * c + 1], Lt[4 * c + 2], Lt[4 * c + 3]);
@@ -882,6 +883,26 @@ struct Dec {
         frontier = A5 + f;
     }
 
+    // TM: the saturated boundary L(S+1) of blocks frozen at a first-pass stage S
+    // whose level lives in registers: after each sweep (and each commit) the
+    // protected rows are set back to +-CAP, so the next sweep's stage S reads
+    // them as the reference does (its inactive stage S+1 PEs never write them).
+    // One place after the sweep instead of a select in every read keeps the
+    // stages' straight-line code free of these rarely taken blocks.
+    template <int SL_ = 0>
+    __device__ __forceinline__ void fixup_regs_from() {
+        if constexpr (SL_ < PL::NLR) {
+            if (prot & (1u << SL_)) {
+                const uint32_t pm = sm->pm[SL_][lane], ss = sm->ss[SL_][lane];
+#pragma unroll
+                for (int j = 0; j < P; ++j)
+                    if ((pm >> j) & 1u) Lr[SL_][j] = ((ss >> j) & 1u) ? -kCap : kCap;
+            }
+            fixup_regs_from<SL_ + 1>();
+        }
+    }
+    __device__ __forceinline__ void fixup_regs() { fixup_regs_from<0>(); }
+
     // apply_freeze (csfg_freeze.cpp:82-93) for the first-pass commits of one
     // iteration (TM, rare: ~1 per frame at 3 dB), kept compact so that it costs
     // little instruction cache when it runs. Commit k (stage S <= 4) covers the
@@ -1087,11 +1108,12 @@ struct Dec {
             PBP_T1(tw, 3);
             PBP_T0(ta);
             int dinact = 0;
-            if (nce_) dinact = apply_early_tm();
+            if (__builtin_expect(nce_ != 0, 0)) dinact = apply_early_tm();
             PBP_T1(ta, 4);
             PBP_T0(tb2);
             if (w.cm) apply_tm(w, dinact);
             if (lane < M) inact += dinact;
+            if (prot & ((1u << PL::NLR) - 1u)) fixup_regs();
             __syncwarp();
             PBP_T1(tb2, PBP_SLOT_APPLY_TM);
         } else {
