@@ -40,6 +40,9 @@ def kernel(rep, frames, iters):
         "registers": m["launch__registers_per_thread"],
         "occupancy_limit_smem_blocks": m["launch__occupancy_limit_shared_mem"],
         "no_instruction_stall_per_issue": m["smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio"],
+        "stalls_per_issue": {k.split("stalled_")[1].replace("_per_issue_active.ratio", ""): round(v, 3)
+                             for k, v in m.items() if k.startswith("smsp__average_warps_issue_stalled_")
+                             and k.endswith("_per_issue_active.ratio") and isinstance(v, float) and v > 0.01},
     }
 
 
@@ -53,8 +56,10 @@ def main():
                   f"gpurun_out/{tag}_prof_*.ncu-rep (not committed); tools/ncu_summary.py",
         "frames_per_launch": frames,
         "csfg": kernel(f"gpurun_out/{tag}_prof_csfg.ncu-rep", frames, arg("--iters-csfg", 25.659)),
-        "baseline": kernel(f"gpurun_out/{tag}_prof_base.ncu-rep", frames, arg("--iters-base", 40.0)),
     }
+    import os
+    if os.path.exists(f"gpurun_out/{tag}_prof_base.ncu-rep"):
+        out["baseline"] = kernel(f"gpurun_out/{tag}_prof_base.ncu-rep", frames, arg("--iters-base", 40.0))
     with open(f"profiles/{tag}_ncu_summary.json", "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps(out, indent=1))
