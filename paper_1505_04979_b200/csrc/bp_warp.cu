@@ -883,6 +883,34 @@ struct Dec {
         frontier = A5 + f;
     }
 
+    // Re-covered rows [start, fr_start) of a commit at stage S (only the first
+    // commit of an iteration can re-cover rows decided before): the top rows
+    // already inactive at a stage s2 > S under their old freeze_stage (fo < s2)
+    // must not be counted twice. Per-lane counts in 16-bit fields of five words
+    // (stages (1,2) .. (9)), one warp sum per word; returns this lane's count
+    // (lane = stage s2).
+    __device__ __forceinline__ int recovered_inactive(int S, int start, int fr_start) const {
+        static_assert(M <= 10, "stages 1..9 in five packed words");
+        uint32_t c[5] = {0u, 0u, 0u, 0u, 0u};
+#pragma unroll 1
+        for (int r = start + lane; r < fr_start; r += 32) {
+            const int fo = sm->fst[r];
+            const int lo = fo > S ? fo : S;
+            const uint32_t top = __brev(~(uint32_t)r) >> (32 - M);  // bit s2: row r is a top row at s2
+            const uint32_t msk = top & ~((2u << lo) - 1u);            // s2 in (max(fo, S), m)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) c[q] += ((msk >> (2 * q + 1)) & 1u) | (((msk >> (2 * q + 2)) & 1u) << 16);
+        }
+        int mine = 0;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const uint32_t t = __reduce_add_sync(kFull, c[q]);
+            if (lane == 2 * q + 1) mine = (int)(t & 0xffffu);
+            if (lane == 2 * q + 2) mine = (int)(t >> 16);
+        }
+        return lane < M ? mine : 0;
+    }
+
     // TM: the saturated boundary L(S+1) of blocks frozen at a first-pass stage S
     // whose level lives in registers: after each sweep (and each commit) the
     // protected rows are set back to +-CAP, so the next sweep's stage S reads
@@ -954,25 +982,7 @@ struct Dec {
             //    re-cover rows decided before (freeze_stage still holds their stages):
             //    those already inactive at s2 are counted once (packed warp sums)
             if (lane > S && lane < M) dinact += sz >> 1;
-            if (k == 0 && start < fr_start) {
-                uint32_t c[5] = {0u, 0u, 0u, 0u, 0u};  // stages (1,2) .. (9): 16-bit fields
-#pragma unroll 1
-                for (int r = start + lane; r < fr_start; r += 32) {
-                    const int fo = sm->fst[r];
-                    const int lo = fo > S ? fo : S;
-                    const uint32_t top = __brev(~(uint32_t)r) >> (32 - M);  // bit s2: top row at s2
-                    const uint32_t msk = top & ~((2u << lo) - 1u);
-#pragma unroll
-                    for (int q = 0; q < 5; ++q)
-                        c[q] += ((msk >> (2 * q + 1)) & 1u) | (((msk >> (2 * q + 2)) & 1u) << 16);
-                }
-#pragma unroll
-                for (int q = 0; q < 5; ++q) {
-                    const uint32_t t = __reduce_add_sync(kFull, c[q]);
-                    if (lane == 2 * q + 1) dinact -= (int)(t & 0xffffu);
-                    if (lane == 2 * q + 2 && lane < M) dinact -= (int)(t >> 16);
-                }
-            }
+            if (k == 0 && start < fr_start) dinact -= recovered_inactive(S, start, fr_start);
             //    freeze_stage over the block (:86), 16 bytes per lane and step
             {
                 const uint32_t w4 = 0x01010101u * (uint32_t)S;
@@ -1213,22 +1223,8 @@ struct Dec {
             // 3. inactive top rows of the stages after S. Only the first commit of
             //    an iteration can re-cover rows decided before (later blocks start
             //    at the frontier), so freeze_stage still holds their old stages.
-            if (k == 0 && start < fr_start) {
-                sm->tmp[lane] = 0;
-                __syncwarp();
-#pragma unroll 1
-                for (int r = start + lane; r < fr_start; r += 32) {
-                    const int fo = sm->fst[r];
-#pragma unroll 1
-                    for (int s2 = S + 1; s2 < M; ++s2)
-                        if (fo < s2 && !((r >> (M - 1 - s2)) & 1)) atomicAdd(&sm->tmp[s2], 1);
-                }
-                __syncwarp();
-                if (lane > S && lane < M) dinact += (sz >> 1) - sm->tmp[lane];
-                __syncwarp();
-            } else if (lane > S && lane < M) {
-                dinact += sz >> 1;
-            }
+            if (lane > S && lane < M) dinact += sz >> 1;
+            if (k == 0 && start < fr_start) dinact -= recovered_inactive(S, start, fr_start);
             //    freeze_stage over the block (csfg_freeze.cpp:86)
             if (sz >= 4) {
                 const uint32_t w4 = 0x01010101u * (uint32_t)S;
