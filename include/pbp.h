@@ -229,8 +229,9 @@ int pbp_kernel_path(int32_t n);
 /* Route every decode of this context through the generic kernel (on != 0).
  * Test hook: lets the suite check both kernels against the oracle. */
 int pbp_ctx_force_generic(pbp_ctx* ctx, int on);
-/* Warp-resident kernel resources for code length n: shared bytes per warp and
- * resident warps per SM (0 when n uses the generic kernel or no device). */
+/* Fast-kernel resources for code length n: shared bytes per warp (warp-resident
+ * kernel, n <= 1024) or per CTA (CTA-per-frame kernel, n = 2048..16384), and resident
+ * warps per SM (0 when n uses the generic kernel only or there is no device). */
 int pbp_kernel_info(int32_t n, int decoder, int32_t* smem_bytes, int32_t* warps_per_sm);
 /* Launch statistics of the last decode on this context (kernel launches,
  * frames re-routed to the generic kernel because |LLR| exceeded the

@@ -38,12 +38,15 @@
 #include <type_traits>
 
 #include "pbp_common.cuh"
+#include "tmem.cuh"
 
 namespace pbp {
 namespace cta {
 
 constexpr unsigned kFull = 0xffffffffu;
-enum : int { kReg = 0, kSmem = 1, kGlob = 2, kBits = 3 };
+// kTmem: a thread-private (inner) level in tensor memory: the thread's P rows are
+// P columns of its TMEM lane (one tcgen05.ld/st per stage instead of P L2 accesses)
+enum : int { kReg = 0, kSmem = 1, kGlob = 2, kBits = 3, kTmem = 4 };
 
 // Per-size plan: threads (LOGT), rows per thread (2^K), where each L level
 // lives, whether R(0) stays in registers, whether Rx is double-buffered.
@@ -53,30 +56,42 @@ template <>
 struct Cfg<11> {  // 128 threads x 16 rows, 3 CTAs per SM: four levels in registers, the rest in shared memory
     static constexpr int LOGT = 7, K = 4, MINB = 3;
     static constexpr bool r0reg = false, rx2 = false;
+    static constexpr int TMEM_COLS = 0;
     static constexpr int where(int s) { return s == 11 ? kBits : (s <= 3 || s == 5) ? kReg : kSmem; }
 };
 template <>
 struct Cfg<12> {  // 256 x 16, two frames per SM: four levels in registers, five in shared memory, two in L2
     static constexpr int LOGT = 8, K = 4, MINB = 2;
     static constexpr bool r0reg = false, rx2 = false;
+    // no TMEM: a kernel that allocates tensor memory gets one CTA per SM
+    // (tools/micro/tmem_occupancy.cu), and n = 4096 needs two frames per SM
+    static constexpr int TMEM_COLS = 0;
     static constexpr int where(int s) {
         return s == 12 ? kBits : (s <= 3 || s == 5) ? kReg : (s == 10 || s == 11) ? kGlob : kSmem;
     }
 };
 template <>
-struct Cfg<13> {  // 512 x 16: three levels in registers, five in shared memory, four in L2
+struct Cfg<13> {  // 512 x 16: three levels in registers, five in shared memory, four in TMEM (all on chip)
     static constexpr int LOGT = 9, K = 4, MINB = 1;
     static constexpr bool r0reg = false, rx2 = false;
+    static constexpr int TMEM_COLS = 512;  // 16 warps: 128 columns of its lane quarter per warp
+    static constexpr bool TPROT_REG = false;
     static constexpr int where(int s) {
-        return s == 13 ? kBits : (s <= 3) ? kReg : (s % 4 == 0 || s == 5 || s == 6) ? kSmem : kGlob;
+        return s == 13 ? kBits : (s <= 3) ? kReg : (s % 4 == 0 || s == 5 || s == 6) ? kSmem : kTmem;
     }
 };
 template <>
-struct Cfg<14> {  // 1024 x 16: one level in shared memory, the rest in L2
+struct Cfg<14> {  // 1024 x 16: one level in shared memory, four in TMEM, the rest in L2
     static constexpr int LOGT = 10, K = 4, MINB = 1;
     static constexpr bool r0reg = false, rx2 = false;
-    // L(12) joins two layouts with lane strides > 1 row (uncoalesced in L2)
-    static constexpr int where(int s) { return s == 14 ? kBits : (s == 12) ? kSmem : kGlob; }
+    static constexpr int TMEM_COLS = 512;  // 32 warps: 64 columns per warp = four levels
+    static constexpr bool TPROT_REG = false;
+    // L(12) joins two layouts with lane strides > 1 row (uncoalesced in L2); the TMEM
+    // levels are inner levels whose blocks freeze rarely (first-pass stages), so their
+    // boundary fix-up after the sweep seldom runs; 148 frames x 8 L2 levels fit the L2
+    static constexpr int where(int s) {
+        return s == 14 ? kBits : (s == 12) ? kSmem : (s == 1 || s == 2 || s == 3 || s == 5) ? kTmem : kGlob;
+    }
 };
 
 template <int M_>
@@ -105,6 +120,15 @@ struct Plan {
     }
     static constexpr int slot(int s) { return count(C::where(s), s); }
     static constexpr int NREG = count(kReg, M + 1), NSM = count(kSmem, M + 1), NGL = count(kGlob, M + 1);
+    static constexpr int NTM = count(kTmem, M + 1);
+    // TMEM: each warp owns TMEM_COLS * 4 / NWARP columns of its lane quarter, P per level
+    static constexpr int TM_WCOLS = C::TMEM_COLS > 0 ? C::TMEM_COLS * 4 / NWARP : 0;
+    static constexpr bool tm_ok() {
+        for (int s = 1; s <= M; ++s)
+            if (C::where(s) == kTmem && !(s < M && s / K == (s - 1) / K)) return false;  // inner levels only
+        return NTM * P <= TM_WCOLS || NTM == 0;
+    }
+    static_assert(tm_ok(), "TMEM levels: thread-private (inner) levels that fit the warp's columns");
     static constexpr int pad(int row) { return row + (row >> 5); }
     static constexpr int NX = N + N / 32;
     // L(s) is produced (stage s) and consumed (stage s-1, commits of stage
@@ -129,6 +153,11 @@ __device__ __forceinline__ uint32_t bits_transform(uint32_t w) {
     return w;
 }
 
+template <int M, typename = void>
+struct TprotReg { static constexpr bool value = false; };
+template <int M>
+struct TprotReg<M, std::void_t<decltype(Cfg<M>::TPROT_REG)>> { static constexpr bool value = Cfg<M>::TPROT_REG; };
+
 template <int M>
 struct Smem {
     using PL = Plan<M>;
@@ -140,6 +169,10 @@ struct Smem {
     uint32_t xh[PL::NW];                           // x_hat = (R(0) + L(0) < 0) of the last sweep
     uint8_t fst[PL::N];                            // freeze_stage per row
     long long frame;
+    // TMEM levels: per thread and level, rows whose L is a frozen-block boundary
+    // (bits 0..P-1) and their signs (bits 16..16+P-1), restored after each sweep
+    uint32_t tprot[(PL::NTM > 0 && !TprotReg<M>::value) ? PL::NTM : 1][(PL::NTM > 0 && !TprotReg<M>::value) ? PL::T : 1];
+    uint32_t tbase;                                // TMEM allocation
 };
 
 // XH: also record each freeze event's x_hat (trace calls; a separate
@@ -154,6 +187,10 @@ struct Dec {
     Smem<M>* sm;
     const DecodeArgs* a;
     float* Lg;  // L2 levels, N floats each
+    uint32_t tb;  // this warp's TMEM columns (TMEM levels at tb + P * slot)
+    static constexpr bool kTpReg = TprotReg<M>::value;
+    uint32_t tpr[kTpReg && PL::NTM > 0 ? PL::NTM : 1];  // boundary masks of the TMEM levels (kTpReg)
+    __device__ __forceinline__ uint32_t& tprot(int k) { return kTpReg ? tpr[k] : sm->tprot[k][tid]; }
     const float* llr;
     int tid, lane, warp;
     float alpha;
@@ -267,11 +304,23 @@ struct Dec {
                 ++k;
             }
         }
+        constexpr bool tin = C::where(S + 1) == kTmem, tout = S > 0 && C::where(S) == kTmem;
+        float tl[tin ? P : 1], to[tout ? P : 1];
+        if constexpr (tin) {
+            tm::wait_st();  // this level's store of the previous sweep / its boundary fix-up
+            tm::ld16(tb + P * PL::slot(S + 1), tl);
+            tm::wait_ld();
+        }
 #pragma unroll
         for (int j = 0, k = 0; j < P; ++j) {
             if (j & dj) continue;
-            lt[k] = ld<S + 1, q>(j);
-            lb[k] = ld<S + 1, q>(j + dj);
+            if constexpr (tin) {
+                lt[k] = tl[j];
+                lb[k] = tl[j + dj];
+            } else {
+                lt[k] = ld<S + 1, q>(j);
+                lb[k] = ld<S + 1, q>(j + dj);
+            }
             ++k;
         }
 #pragma unroll
@@ -287,7 +336,12 @@ struct Dec {
             const float sum_bot = __fadd_rn(lb[k], r_b);
             const float l_top = __fmul_rn(alpha, xsmin(lt[k], sum_bot));
             const float l_bot = __fadd_rn(lb[k], cross);
-            if constexpr (S > 0) {
+            if constexpr (tout) {
+                // every PE's outputs (an inactive PE's only matter at a frozen block's
+                // boundary L, which fixup_tmem restores after the sweep)
+                to[j] = l_top;
+                to[j + dj] = l_bot;
+            } else if constexpr (S > 0) {
                 if (on) {
                     st<S, q>(j, l_top);
                     st<S, q>(j + dj, l_bot);
@@ -310,6 +364,7 @@ struct Dec {
             }
             ++k;
         }
+        if constexpr (tout) tm::st16(tb + P * PL::slot(S), to);
         act += __popc(onb);
         if constexpr (csfg) {
             onm |= onb << (i * (P / 2));
@@ -486,6 +541,10 @@ struct Dec {
             } else if constexpr (wl == kBits) {
                 lm_nz |= bm;
                 lm_neg = (lm_neg & ~bm) | (x & bm);
+            } else if constexpr (wl == kTmem) {  // written into TMEM by fixup_tmem after the sweep
+                uint32_t& w = tprot(PL::slot(S + 1));
+                w = (w | bm) & ~(bm << 16);
+                w |= (x & bm) << 16;
             }
 #pragma unroll 1
             for (uint32_t left = bm; left; left &= left - 1u) {
@@ -526,6 +585,26 @@ struct Dec {
             act -= __popc(drop);
             onm &= ~drop;
             uncount<q, i + 1>(bm, all);
+        }
+    }
+
+    // TMEM levels: the saturated boundary L(S+1) of blocks frozen at stage S,
+    // overwritten by their (inactive) stage-S+1 PEs in this sweep, set back to
+    // +-CAP before the next sweep's stage S reads it (csfg_freeze.cpp:84-86)
+    template <int K_ = 0>
+    __device__ __forceinline__ void fixup_tmem() {
+        if constexpr (K_ < PL::NTM) {
+            const uint32_t w = tprot(K_);
+            if (__any_sync(kFull, w != 0u)) {
+                float v[P];
+                tm::ld16(tb + P * K_, v);
+                tm::wait_ld();
+#pragma unroll
+                for (int j = 0; j < P; ++j)
+                    if ((w >> j) & 1u) v[j] = ((w >> (16 + j)) & 1u) ? -kCap : kCap;
+                tm::st16(tb + P * K_, v);
+            }
+            fixup_tmem<K_ + 1>();
         }
     }
 
@@ -607,6 +686,16 @@ struct Dec {
             for (int j = 0; j < P; ++j) R[j] = 0.f;  // R(m) = 0 until the first sweep (max_iter = 0)
             for (int i = tid; i < PL::NSM * PL::NX; i += kT) (&sm->Ls[0][0])[i] = 0.f;
             for (int i = tid; i < PL::NGL * N; i += kT) Lg[i] = 0.f;
+            if constexpr (PL::NTM > 0) {
+                float z[P];
+#pragma unroll
+                for (int j = 0; j < P; ++j) z[j] = 0.f;
+#pragma unroll
+                for (int k = 0; k < PL::NTM; ++k) {
+                    tm::st16(tb + P * k, z);
+                    tprot(k) = 0u;
+                }
+            }
             for (int r = tid; r < N; r += kT) sm->fst[r] = kNotFrozen;
             for (int w = tid; w < NW; w += kT) sm->dec[w] = 0u;
             frontier = 0;
@@ -633,6 +722,7 @@ struct Dec {
                     else R[j] = __fadd_rn(llr[row<0>(j)], 0.0f);
                 }
                 sweep_from<0>();
+                if constexpr (csfg && PL::NTM > 0) fixup_tmem();
                 if constexpr (KIND == 0) {
                     __syncthreads();  // Rx buffers are reused by the next sweep
                 } else if constexpr (KIND == 1) {
@@ -704,7 +794,23 @@ template <int M, int KIND, bool XH = false>
 __global__ void __launch_bounds__(Plan<M>::T, Cfg<M>::MINB) bp_cta_kernel(const __grid_constant__ DecodeArgs a) {
     extern __shared__ __align__(16) unsigned char csm[];
     Dec<M, KIND, XH> dec;
-    dec.run(a, reinterpret_cast<Smem<M>*>(csm));
+    Smem<M>* sm = reinterpret_cast<Smem<M>*>(csm);
+    if constexpr (Plan<M>::NTM > 0) {
+        constexpr int COLS = Cfg<M>::TMEM_COLS;
+        const int warp = threadIdx.x >> 5;
+        if (warp == 0) tm::alloc<COLS>(&sm->tbase);
+        tm::fence_before();
+        __syncthreads();
+        tm::fence_after();
+        dec.tb = sm->tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(Plan<M>::TM_WCOLS * (warp >> 2));
+        dec.run(a, sm);
+        tm::fence_before();
+        __syncthreads();
+        tm::fence_after();
+        if (warp == 0) tm::dealloc<COLS>(sm->tbase);
+    } else {
+        dec.run(a, sm);
+    }
 }
 
 template <int M, int KIND, bool XH>
@@ -773,6 +879,18 @@ cudaError_t launch_cta(const DecodeArgs& a, int grid, cudaStream_t st) {
     }
     return cudaErrorInvalidValue;
 }
+
+size_t cta_smem_bytes(int m) {
+    switch (m) {
+        case 11: return sizeof(cta::Smem<11>);
+        case 12: return sizeof(cta::Smem<12>);
+        case 13: return sizeof(cta::Smem<13>);
+        case 14: return sizeof(cta::Smem<14>);
+    }
+    return 0;
+}
+
+int cta_warps(int m) { return m >= 11 && m <= 14 ? 1 << (m - 4 - 5) : 0; }  // 16 rows per thread
 
 int cta_blocks_per_sm(int m, int kind) {
     switch (m) {

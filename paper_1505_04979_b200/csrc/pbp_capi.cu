@@ -30,6 +30,8 @@ int cta_kernel_supported(int m);
 long long cta_scratch_floats(int m);
 cudaError_t launch_cta(const DecodeArgs& a, int grid, cudaStream_t st);
 int cta_blocks_per_sm(int m, int kind);
+size_t cta_smem_bytes(int m);
+int cta_warps(int m);
 cudaError_t launch_channel(const GenArgs& g, int grid, cudaStream_t stream);
 }  // namespace pbp
 
@@ -533,9 +535,17 @@ int pbp_ctx_synchronize(pbp_ctx* ctx) {
 int pbp_kernel_info(int32_t n, int decoder, int32_t* smem_bytes, int32_t* warps_per_sm) {
     if (!is_pow2(n)) return fail(PBP_EINVAL, "pbp_kernel_info: n must be a power of two");
     const int m = log2i(n);
-    if (smem_bytes) *smem_bytes = pbp::warp_kernel_supported(m) ? (int32_t)pbp::warp_smem_bytes(m, decoder) : 0;
-    if (warps_per_sm)
-        *warps_per_sm = pbp::warp_kernel_supported(m) ? pbp::warp_blocks_per_sm(m, decoder) * pbp::warp_kernel_warps(m) : 0;
+    if (decoder < 0 || decoder > 2) return fail(PBP_EINVAL, "unknown decoder kind");
+    if (pbp::warp_kernel_supported(m)) {
+        if (smem_bytes) *smem_bytes = (int32_t)pbp::warp_smem_bytes(m, decoder);
+        if (warps_per_sm) *warps_per_sm = pbp::warp_blocks_per_sm(m, decoder) * pbp::warp_kernel_warps(m);
+    } else if (pbp::cta_kernel_supported(m)) {  // CTA per frame: shared bytes per CTA, resident warps
+        if (smem_bytes) *smem_bytes = (int32_t)pbp::cta_smem_bytes(m);
+        if (warps_per_sm) *warps_per_sm = pbp::cta_blocks_per_sm(m, decoder) * pbp::cta_warps(m);
+    } else {
+        if (smem_bytes) *smem_bytes = 0;
+        if (warps_per_sm) *warps_per_sm = 0;
+    }
     return PBP_OK;
 }
 
