@@ -920,11 +920,13 @@ struct Dec {
     template <int SL_ = 0>
     __device__ __forceinline__ void fixup_regs_from() {
         if constexpr (SL_ < PL::NLR) {
-            if (prot & (1u << SL_)) {
+            if (__any_sync(kFull, prot & (1u << SL_))) {  // warp-uniform: no reconvergence stack
                 const uint32_t pm = sm->pm[SL_][lane], ss = sm->ss[SL_][lane];
 #pragma unroll
-                for (int j = 0; j < P; ++j)
-                    if ((pm >> j) & 1u) Lr[SL_][j] = ((ss >> j) & 1u) ? -kCap : kCap;
+                for (int j = 0; j < P; ++j) {  // selects, not branches
+                    const float sat = __uint_as_float(__float_as_uint(kCap) | (((ss >> j) & 1u) << 31));
+                    Lr[SL_][j] = ((pm >> j) & 1u) ? sat : Lr[SL_][j];
+                }
             }
             fixup_regs_from<SL_ + 1>();
         }
@@ -1085,20 +1087,21 @@ struct Dec {
         }
         // inactive top rows: a stage-S block of B rows has B/2 top rows at every later stage
         if (lane < M) dinact += (int)((__brev((cm << 5) & ((1u << lane) - 1u)) >> (32 - M)) >> 1);
-        if ((cm >> lane) & 1u) {
-            const int S = 5 + lane, B = 16 >> lane, A = w.Al;
-            const uint32_t wm = (1u << B) - 1u;
-            if (lane < 4) atomicOr(&sm->pm[PL::NLR + lane][A >> 5], wm << (A & 31));  // L(S+1): shared slot S - 5
+        const bool mine = (cm >> lane) & 1u;
+        const int B = 16 >> lane, A = w.Al;
+        const uint32_t wm = (1u << B) - 1u;
+        if (mine && lane < 4) atomicOr(&sm->pm[PL::NLR + lane][A >> 5], wm << (A & 31));  // L(S+1): shared slot S - 5
+        if (a->events) {  // trace calls only (uniform)
             const int e_ix = nev + __popc(cm & ((1u << lane) - 1u));
-            if (a->events && e_ix < a->ev_cap) {
+            if (mine && e_ix < a->ev_cap) {
                 int* e = a->events + ((long long)frame_ * a->ev_cap + e_ix) * 5;
                 e[0] = it;
-                e[1] = S;
+                e[1] = 5 + lane;
                 e[2] = A >> (4 - lane);
                 e[3] = A;
                 e[4] = B;
             }
-            if (XH && a->ev_xhat && e_ix < a->ev_cap)  // the block is <= 16 aligned rows
+            if (XH && a->ev_xhat && mine && e_ix < a->ev_cap)  // the block is <= 16 aligned rows
                 atomicOr(&a->ev_xhat[((long long)frame_ * a->ev_cap + e_ix) * NW + (A >> 5)],
                          ((w.xl >> (A - A5)) & wm) << (A & 31));
         }
