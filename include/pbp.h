@@ -199,6 +199,14 @@ int pbp_decode_count_device(pbp_ctx* ctx, const pbp_code* code, int decoder,
                             const float* llrs_dev, const uint32_t* u_dev, int64_t frames,
                             float alpha, int32_t max_iter, int64_t* counters_dev, void* stream);
 
+/* As pbp_decode_count_device with one counter set per `batch` consecutive frames
+ * (counters_dev: ceil(frames / batch) x 10 int64, accumulated): e.g. a whole Eb/N0
+ * sweep stored point after point, decoded in ONE launch with per-point counters. */
+int pbp_decode_count_batches_device(pbp_ctx* ctx, const pbp_code* code, int decoder,
+                                    const float* llrs_dev, const uint32_t* u_dev, int64_t frames,
+                                    int64_t batch, float alpha, int32_t max_iter,
+                                    int64_t* counters_dev, void* stream);
+
 /* run_point's batches (src/sim_harness.cpp:136-178, kBatchSize = 256 at :21): trials
  * [first_trial, first_trial + frames) generated and decoded as pbp_simulate_point does
  * (fp64 != 0: the reference's double LLRs decoded in double), with ONE counter set per

@@ -418,6 +418,10 @@ def simulate_sweep_multi(code: PolarCode, decoder, seed: int, frames_per_point: 
     devs = list(range(device_count())) if devices is None else [int(d) for d in devices]
     if not devs:
         raise RuntimeError("simulate_sweep_multi: no CUDA device")
+    try:  # libpbp.so resolves NCCL at first use: let it bind to torch's copy (a newer
+        import torch  # noqa: F401  NCCL than the system one, which torch cannot load over)
+    except ImportError:
+        pass
     dv = (C.c_int * len(devs))(*devs)
     sv = (C.c_double * len(snrs))(*[float(x) for x in snrs])
     out = (_abi.PbpCounters * len(snrs))()

@@ -102,6 +102,9 @@ SIGNATURES = {
     "pbp_simulate_sweep_multi": (C.c_int, [C.POINTER(C.c_int), C.c_int, _CP, C.c_int, C.c_uint64, C.c_int64,
                                            C.POINTER(C.c_double), C.c_int, C.c_int, C.c_float, C.c_int32,
                                            C.POINTER(PbpCounters)]),
+    "pbp_decode_count_batches_device": (C.c_int, [_P, _CP, C.c_int, C.POINTER(C.c_float),
+                                                  C.POINTER(C.c_uint32), C.c_int64, C.c_int64, C.c_float,
+                                                  C.c_int32, C.POINTER(C.c_int64), _P]),
     "pbp_kernel_path": (C.c_int, [C.c_int32]),
     "pbp_ctx_force_generic": (C.c_int, [_P, C.c_int]),
     "pbp_kernel_info": (C.c_int, [C.c_int32, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),

@@ -230,6 +230,7 @@ struct Dec {
     bool done_;    // the frontier reached n
     uint32_t prot;   // bit per protection slot: some lane holds a frozen-boundary row
     long long act, frame_;
+    long long cset_;  // counter set sm->cnt accumulates (cnt_batch > 0)
     uint32_t xq;     // channel-side decisions of stage 0, permuted pass-0 layout
     int xperm;       // lane holding row-order word `lane` of x_hat after transpose
 
@@ -1548,6 +1549,7 @@ struct Dec {
             xperm = P - 1 - p;
         }
         if (lane < kNumCounters) sm->cnt[lane] = 0ull;
+        cset_ = 0;
         __syncwarp();
 
         for (;;) {
@@ -1612,7 +1614,7 @@ struct Dec {
             write_outputs(f, uw, iters, stop);
         }
         if (args.counters && lane < kNumCounters && sm->cnt[lane])
-            atomicAdd(&args.counters[lane], sm->cnt[lane]);
+            atomicAdd(&args.counters[cset_ * kNumCounters + lane], sm->cnt[lane]);
 #ifdef PBP_PROF_SECTIONS
         if (lane == 0)
             for (int i = 0; i < 8; ++i) atomicAdd(&g_prof[i], prof[i]);
@@ -1646,11 +1648,19 @@ struct Dec {
                 case kCntStop2: v = stop == 2; break;
                 default: break;
             }
+            // a warp's frames come from the queue in increasing order: accumulate
+            // locally while they stay in one counter set, flush when the set changes
             if (args.cnt_batch > 0) {
-                if (lane < kNumCounters && v) atomicAdd(&counter_set(args, f)[lane], v);
-            } else if (lane < kNumCounters) {
-                sm->cnt[lane] += v;
+                const long long set = f / args.cnt_batch;
+                if (set != cset_) {
+                    if (lane < kNumCounters && sm->cnt[lane]) {
+                        atomicAdd(&args.counters[cset_ * kNumCounters + lane], sm->cnt[lane]);
+                        sm->cnt[lane] = 0ull;
+                    }
+                    cset_ = set;
+                }
             }
+            if (lane < kNumCounters) sm->cnt[lane] += v;
         }
     }
 

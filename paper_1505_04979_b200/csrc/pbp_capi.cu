@@ -1012,6 +1012,28 @@ int pbp_decode_count_device(pbp_ctx* ctx, const pbp_code* code, int decoder, con
     return run_decode(ctx, r, next_slot(ctx), pick(ctx, stream));
 }
 
+int pbp_decode_count_batches_device(pbp_ctx* ctx, const pbp_code* code, int decoder, const float* llrs_dev,
+                                    const uint32_t* u_dev, int64_t frames, int64_t batch, float alpha,
+                                    int32_t max_iter, int64_t* counters_dev, void* stream) {
+    if (!ctx) return fail(PBP_EINVAL, "null context");
+    if (!counters_dev || !u_dev) return fail(PBP_EINVAL, "pbp_decode_count_batches_device: null counters or u");
+    if (batch < 1 || batch > 0x7fffffff) return fail(PBP_EINVAL, "pbp_decode_count_batches_device: batch out of range");
+    PBP_CUDA(cudaSetDevice(ctx->device));
+    int rc = upload_code(ctx, code);
+    if (rc) return rc;
+    DecodeReq r;
+    r.kind = decoder;
+    r.llr = llrs_dev;
+    r.frames = frames;
+    r.alpha = alpha;
+    r.max_iter = max_iter;
+    r.truth = u_dev;
+    r.counters = reinterpret_cast<unsigned long long*>(counters_dev);
+    r.cnt_batch = (int)batch;
+    if ((rc = begin_call(ctx, 1))) return rc;
+    return run_decode(ctx, r, next_slot(ctx), pick(ctx, stream));
+}
+
 // run_point's trial loop on the device: fp32 LLRs (the fast path) or, with
 // f64, the reference's double LLRs decoded in double.
 static int simulate_point_impl(pbp_ctx* ctx, const pbp_code* code, int decoder, uint64_t seed,

@@ -14,6 +14,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -35,8 +36,17 @@ const Nccl& nccl() {
     static Nccl n;
     static std::once_flag once;
     std::call_once(once, [] {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        // an NCCL the process already loaded (torch's) first, then PBP_NCCL_LIB, then
+        // the loader's search path. A copy loaded here owns the soname libnccl.so.2
+        // for the rest of the process: a later `import torch` would bind to it, so
+        // the Python wrapper imports torch before the first call.
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) {
+            const char* env = std::getenv("PBP_NCCL_LIB");
+            if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+        }
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
         if (!h) {
             const char* e = dlerror();
             n.err = std::string("libnccl.so.2 not loadable: ") + (e ? e : "?");

@@ -77,3 +77,33 @@ def test_run_point_stop_rule_matches_batchwise_oracle(ctx):
                 if fe["gmatrix"][b - 1] >= 40 and fe["csfg"][b - 1] >= 40)
     assert stop == frames
     assert rows[0].frame_errors == fe["gmatrix"][-1] and rows[1].frame_errors == fe["csfg"][-1]
+
+
+@pytest.mark.parametrize("n", [1024, 4096])
+def test_decode_count_batches_one_launch_per_sweep(ctx, n):
+    """pbp_decode_count_batches_device over a sweep stored point after point (bench.py's
+    timed launch): one counter set per point, equal to each point's simulate_point."""
+    import ctypes as C
+    import torch
+    code = P.PolarCode.construct(n, n // 2, Z0)
+    snrs, frames = [1.5, 2.5, 3.5], 700 if n == 1024 else 300
+    llr = np.concatenate([P.generate(code, 2, 50, frames, s, ctx=ctx)[0] for s in snrs])
+    u = np.concatenate([P.generate(code, 2, 50, frames, s, ctx=ctx)[1] for s in snrs])
+    dev = torch.device("cuda", ctx.device)
+    d_llr = torch.from_numpy(llr).to(dev)
+    d_u = torch.from_numpy(u.view(np.int32)).to(dev)
+    cnt = torch.zeros((len(snrs), 10), dtype=torch.int64, device=dev)
+    cs = code.c_struct()
+    torch.cuda.synchronize(dev)
+    P._check(P.lib.pbp_decode_count_batches_device(ctx.handle, C.byref(cs), 2, P._abi.f32p(d_llr.data_ptr()),
+                                                   P._abi.u32p(d_u.data_ptr()), len(snrs) * frames, frames,
+                                                   0.9375, 40, P._abi.i64p(cnt.data_ptr()), None))
+    ctx.synchronize()
+    got = cnt.cpu().numpy()
+    for i, s in enumerate(snrs):
+        want = P.simulate_point(code, "csfg", 2, 50, frames, s, ctx=ctx)
+        assert [int(x) for x in got[i]] == [want[k] for k in COUNTER_FIELDS]
+    with pytest.raises(ValueError):
+        P._check(P.lib.pbp_decode_count_batches_device(ctx.handle, C.byref(cs), 2, P._abi.f32p(d_llr.data_ptr()),
+                                                       P._abi.u32p(d_u.data_ptr()), frames, 0, 0.9375, 40,
+                                                       P._abi.i64p(cnt.data_ptr()), None))
