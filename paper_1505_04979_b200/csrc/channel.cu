@@ -6,9 +6,12 @@
 //   rows in ascending order and encoded (polar_code.cpp:82-91);
 //   then per symbol two draws -> Box-Muller cosine branch (channel.cpp:34-39),
 //   y = s + sigma * g, LLR = (2/sigma^2) * y in fp64 (channel.cpp:49-60).
-// One warp per trial: lane 0 seeds the 312-word state (inherently serial),
-// the twist runs warp-parallel in the three phases of libstdc++'s
-// _M_gen_rand, tempering and consumption are lane-parallel. Integer state is
+// Seeding the 312-word state is a serial recurrence per trial, so it runs
+// lane-per-trial in channel_seed_kernel (32 trials per warp, states written
+// trial-major to a scratch through a shared-memory transpose); the generation
+// kernel then runs one warp per trial: coalesced state load, the twist
+// warp-parallel in the three phases of libstdc++'s _M_gen_rand, tempering and
+// consumption lane-parallel. Integer state is
 // bit-exact; the fp64 log/cos are CUDA's (<= 2 ulp), which the parity tests
 // compare against glibc on the host (fp32 LLRs are what the decoder sees).
 #include "pbp_common.cuh"
@@ -100,6 +103,35 @@ __device__ __forceinline__ double box_muller(unsigned long long d1, unsigned lon
 
 }  // namespace
 
+// std::mt19937_64 seeding (x_i = 6364136223846793005 (x ^ x >> 62) + i) of
+// TrialRng(seed, first + t) for t < count, one lane per trial; mt_out[t][312].
+// Each lane produces 8 words at a time into a padded shared tile, then the warp
+// stores 4 trials x 64 contiguous bytes per instruction.
+__global__ void __launch_bounds__(kGenWarps * 32) channel_seed_kernel(unsigned long long seed, long long first,
+                                                                       long long count, unsigned long long* mt_out) {
+    __shared__ unsigned long long tile[kGenWarps][32][9];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long t0 = ((long long)blockIdx.x * kGenWarps + warp) * 32;
+    if (t0 >= count) return;
+    const unsigned long long trial = (unsigned long long)(first + t0 + lane);
+    unsigned long long x = mix64(seed + 0x9E3779B97F4A7C15ull * (trial + 1ull));
+    auto& tl = tile[warp];
+    for (int i0 = 0; i0 < kMtN; i0 += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (i0 + j > 0) x = 6364136223846793005ull * (x ^ (x >> 62)) + (unsigned long long)(i0 + j);
+            tl[lane][j] = x;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int tt = 4 * q + (lane >> 3), j = lane & 7;
+            if (t0 + tt < count) mt_out[(t0 + tt) * kMtN + i0 + j] = tl[tt][j];
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void __launch_bounds__(kGenWarps * 32) channel_gen_kernel(GenArgs g) {
     extern __shared__ unsigned long long gsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -114,15 +146,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) channel_gen_kernel(GenArgs g) 
     const int draws = g.k + 2 * g.n;
 
     for (long long it = (long long)blockIdx.x * kGenWarps + warp; it < g.count; it += total_warps) {
-        const unsigned long long trial = (unsigned long long)(g.first + it);
-        if (lane == 0) {
-            unsigned long long x = mix64(g.seed + 0x9E3779B97F4A7C15ull * (trial + 1ull));
-            mt[0] = x;
-            for (int i = 1; i < kMtN; ++i) {
-                x = 6364136223846793005ull * (x ^ (x >> 62)) + (unsigned long long)i;
-                mt[i] = x;
-            }
-        }
+        for (int i = lane; i < kMtN; i += 32) mt[i] = __ldcs(g.mt0 + it * kMtN + i);
         for (int q = lane; q < nw; q += 32) uw[q] = 0u;
         __syncwarp();
         bool encoded = false;
@@ -182,7 +206,16 @@ size_t channel_smem_bytes(int n) {
     return (size_t)kGenWarps * (2 * kMtN + 1) * 8 + (size_t)kGenWarps * 2 * nw * 4;
 }
 
+long long channel_seed_words(long long count) { return count * kMtN; }
+
 cudaError_t launch_channel(const GenArgs& g, int grid, cudaStream_t stream) {
+    {
+        const long long warps = (g.count + 31) / 32;
+        channel_seed_kernel<<<(unsigned)((warps + kGenWarps - 1) / kGenWarps), kGenWarps * 32, 0, stream>>>(
+            g.seed, g.first, g.count, g.mt0);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     const size_t smem = channel_smem_bytes(g.n);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(channel_gen_kernel,

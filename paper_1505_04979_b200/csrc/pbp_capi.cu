@@ -33,6 +33,7 @@ int cta_blocks_per_sm(int m, int kind);
 size_t cta_smem_bytes(int m);
 int cta_warps(int m);
 cudaError_t launch_channel(const GenArgs& g, int grid, cudaStream_t stream);
+long long channel_seed_words(long long count);
 }  // namespace pbp
 
 namespace {
@@ -99,6 +100,7 @@ struct DecodeSlot {
     DevBuf<float> gen_llr;
     DevBuf<double> gen_llr64;
     DevBuf<uint32_t> gen_truth;
+    DevBuf<unsigned long long> gen_mt;  // seeded mt19937_64 states of one generation piece
 };
 constexpr int kSlots = 3;
 
@@ -409,7 +411,12 @@ int run_generic_list(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream
     return PBP_OK;
 }
 
-int run_generate(pbp_ctx* ctx, uint64_t seed, long long first, long long count, double ebn0,
+// trials per seeding piece: 2.5 KB of state each (80 MiB per piece)
+constexpr long long kGenPiece = 32768;
+
+// generation into the given buffers on st, with the slot's seed scratch (the
+// caller orders st after the slot's previous use)
+int run_generate(pbp_ctx* ctx, DecodeSlot& sl, uint64_t seed, long long first, long long count, double ebn0,
                  int noiseless, float* llr, double* llr64, uint32_t* u, cudaStream_t st) {
     if (count < 0) return fail(PBP_EINVAL, "count < 0");
     double sigma2 = 0.0;
@@ -428,10 +435,22 @@ int run_generate(pbp_ctx* ctx, uint64_t seed, long long first, long long count, 
     g.info_rows = ctx->info_rows.p;
     g.llr = llr;
     g.llr64 = llr64;
-    g.u_out = u;
-    const long long grid = std::min<long long>((count + 3) / 4, (long long)ctx->sm_count * 8);
-    cudaError_t e = pbp::launch_channel(g, (int)std::max<long long>(grid, 1), st);
-    if (e != cudaSuccess) return cuda_fail(e, "channel_gen_kernel launch");
+    const long long piece = std::min(count, kGenPiece);
+    int rc = sl.gen_mt.ensure((size_t)pbp::channel_seed_words(piece));
+    if (rc) return rc;
+    g.mt0 = sl.gen_mt.p;
+    const int nw = (ctx->n + 31) / 32;
+    for (long long done = 0; done < count; done += piece) {
+        const long long c = std::min(piece, count - done);
+        g.first = first + done;
+        g.count = c;
+        g.llr = llr ? llr + done * ctx->n : nullptr;
+        g.llr64 = llr64 ? llr64 + done * ctx->n : nullptr;
+        g.u_out = u ? u + done * nw : nullptr;
+        const long long grid = std::min<long long>((c + 3) / 4, (long long)ctx->sm_count * 8);
+        cudaError_t e = pbp::launch_channel(g, (int)std::max<long long>(grid, 1), st);
+        if (e != cudaSuccess) return cuda_fail(e, "channel_gen_kernel launch");
+    }
     return PBP_OK;
 }
 
@@ -505,6 +524,7 @@ int pbp_ctx_destroy(pbp_ctx* ctx) {
         ctx->slot[i].gen_llr.release();
         ctx->slot[i].gen_llr64.release();
         ctx->slot[i].gen_truth.release();
+        ctx->slot[i].gen_mt.release();
     }
     ctx->rerouted.release();
     ctx->blist.release();
@@ -956,8 +976,13 @@ int pbp_generate_device(pbp_ctx* ctx, const pbp_code* code, uint64_t seed, int64
     PBP_CUDA(cudaSetDevice(ctx->device));
     int rc = upload_code(ctx, code);
     if (rc) return rc;
-    return run_generate(ctx, seed, first_trial, count, ebn0_db, noiseless, llr_dev, llr64_dev, u_dev,
-                        pick(ctx, stream));
+    DecodeSlot& sl = next_slot(ctx);
+    cudaStream_t st = pick(ctx, stream);
+    PBP_CUDA(cudaStreamWaitEvent(st, sl.done, 0));  // the slot's seed scratch
+    rc = run_generate(ctx, sl, seed, first_trial, count, ebn0_db, noiseless, llr_dev, llr64_dev, u_dev, st);
+    if (rc) return rc;
+    PBP_CUDA(cudaEventRecord(sl.done, st));
+    return PBP_OK;
 }
 
 int pbp_generate(pbp_ctx* ctx, const pbp_code* code, uint64_t seed, int64_t first_trial, int64_t count,
@@ -974,7 +999,13 @@ int pbp_generate(pbp_ctx* ctx, const pbp_code* code, uint64_t seed, int64_t firs
     PBP_CUDA(cudaMalloc(&d_llr, std::max<size_t>(1, (size_t)count * n * 4)));
     if (llr64) PBP_CUDA(cudaMalloc(&d_llr64, std::max<size_t>(1, (size_t)count * n * 8)));
     if (u_bits) PBP_CUDA(cudaMalloc(&d_u, std::max<size_t>(1, (size_t)count * nw * 4)));
-    rc = run_generate(ctx, seed, first_trial, count, ebn0_db, noiseless, d_llr, d_llr64, d_u, ctx->stream);
+    DecodeSlot& sl = next_slot(ctx);
+    PBP_CUDA(cudaStreamWaitEvent(ctx->stream, sl.done, 0));
+    rc = run_generate(ctx, sl, seed, first_trial, count, ebn0_db, noiseless, d_llr, d_llr64, d_u, ctx->stream);
+    if (!rc) {
+        cudaError_t e = cudaEventRecord(sl.done, ctx->stream);
+        if (e != cudaSuccess) rc = cuda_fail(e, "pbp_generate");
+    }
     if (!rc && count > 0) {
         cudaStream_t st = ctx->stream;
         if (llr) cudaMemcpyAsync(llr, d_llr, (size_t)count * n * 4, cudaMemcpyDeviceToHost, st);
@@ -1060,7 +1091,7 @@ static int simulate_point_impl(pbp_ctx* ctx, const pbp_code* code, int decoder, 
     for (long long done = 0; done < frames; done += chunk) {
         const long long c = std::min(chunk, frames - done);
         PBP_CUDA(cudaStreamWaitEvent(st, sl.done, 0));  // the slot's previous decode read the staging
-        if ((rc = run_generate(ctx, seed, first_trial + done, c, ebn0_db, noiseless, sl.gen_llr.p,
+        if ((rc = run_generate(ctx, sl, seed, first_trial + done, c, ebn0_db, noiseless, sl.gen_llr.p,
                                f64 ? sl.gen_llr64.p : nullptr, sl.gen_truth.p, st)))
             return rc;
         DecodeReq r;

@@ -70,6 +70,7 @@ struct GenArgs {
     float* llr;            // count x n (nullable)
     double* llr64;         // count x n (nullable)
     uint32_t* u_out;       // count x ceil(n/32) (nullable)
+    unsigned long long* mt0;  // count x 312 scratch: the seeded mt19937_64 states
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
