@@ -436,7 +436,7 @@ int run_generate(pbp_ctx* ctx, DecodeSlot& sl, uint64_t seed, long long first, l
     g.llr = llr;
     g.llr64 = llr64;
     const long long piece = std::min(count, kGenPiece);
-    int rc = sl.gen_mt.ensure((size_t)pbp::channel_seed_words(piece));
+    rc = sl.gen_mt.ensure((size_t)pbp::channel_seed_words(piece));
     if (rc) return rc;
     g.mt0 = sl.gen_mt.p;
     const int nw = (ctx->n + 31) / 32;
