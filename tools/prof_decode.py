@@ -43,7 +43,7 @@ for r in range(a.reps):
           f"PE/s {c[5]/dt:.3e}  ({c[5]*9/dt/1e12:.2f} TOP/s)")
 if hasattr(P.lib, "pbp_prof_read") and os.environ.get("PBP_LIB"):
     # library built with -DPBP_PROF_SECTIONS: per-warp clock64 split of the last rep
-    buf = (C.c_ulonglong * 8)()
+    buf = (C.c_ulonglong * 16)()
     P.lib.pbp_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
     P.lib.pbp_prof_read(buf, 1)
     cnt.zero_()
@@ -57,3 +57,7 @@ if hasattr(P.lib, "pbp_prof_read") and os.environ.get("PBP_LIB"):
     its = cnt.cpu().tolist()[3]
     for i, nm in enumerate(names):
         print(f"  {nm:12s} {buf[i]/tot*100:6.1f}%  {buf[i]/its:9.1f} clk/iter")
+    if buf[15]:  # warp-specialised kernel: sweep-warp slots above (5 = wait for B, 4 = export), bookkeeping here
+        for i, nm in enumerate(["wait C", "walk_tm", "apply_tm", "gcheck", "", "", "", "total"]):
+            if nm:
+                print(f"  bk {nm:9s} {buf[8 + i]/buf[15]*100:6.1f}%  {buf[8 + i]/its:9.1f} clk/iter")
