@@ -36,7 +36,6 @@
 // (read-side override for register arrays, predicated stores for shared
 // slots, re-saturation for X). PE activations are counted by the reference
 // rule from per-stage inactive-row counts.
-#include <cstdlib>
 #include <type_traits>
 
 #include "pbp_common.cuh"
@@ -179,11 +178,11 @@ __device__ __forceinline__ uint32_t jmask(int tp) {
 
 #ifdef PBP_PROF_SECTIONS
 // timing experiments only: per-warp clock64 time per code section
-__device__ unsigned long long g_prof[16];  // 8..15: bookkeeping warps of the warp-specialised kernel
+__device__ unsigned long long g_prof[8];
 extern "C" int pbp_prof_read(unsigned long long* out, int reset) {
     if (cudaMemcpyFromSymbol(out, g_prof, sizeof(g_prof)) != cudaSuccess) return 1;
     if (reset) {
-        unsigned long long z[16] = {};
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         cudaMemcpyToSymbol(g_prof, z, sizeof(z));
     }
     return 0;
@@ -198,26 +197,9 @@ extern "C" int pbp_prof_read(unsigned long long* out, int reset) {
 #define PBP_T1(v, k)
 #endif
 
-// Handoff between the two warps of one frame slot in the warp-specialised
-// n = 1024 csfg kernel (bp_ws_kernel): C = "sweep t exported" (sweep warp ->
-// bookkeeping warp), B = "iteration t booked" (bookkeeping -> sweep warp).
-struct alignas(16) WsHand {
-    unsigned long long mbC, mbB;
-    // C: sweep t's first-pass walk (walk0) and its commits' side effects
-    int frame, it, nce, s_last, done, frontier, L1, fr_start;
-    // B: the iteration's outcome
-    int bdone, bfrontier;
-    int dinact[16];   // apply_early_tm's newly inactive top rows per stage (lanes < m)
-    uint32_t xq[32];  // stage-0 channel-side decisions (x_hat), permuted pass-0 layout
-};
-
 // XH: also record each freeze event's x_hat (trace calls; a separate
-// instantiation keeps the decode kernel's code unchanged).
-// ROLE: 0 = one warp decodes the frame (all kernels); n = 1024 csfg
-// warp-specialised pair: 1 = sweep warp (stage math, snapshots, first-pass
-// walk and commits), 2 = bookkeeping warp (last-pass walk and commits, PE
-// counts, G-check, outputs), overlapping the sweep warp's next sweep.
-template <int M, int KIND, bool XH = false, int ROLE = 0>
+// instantiation keeps the decode kernel's code unchanged)
+template <int M, int KIND, bool XH = false>
 struct Dec {
 #ifdef PBP_PROF_SECTIONS
     unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -228,8 +210,6 @@ struct Dec {
     using Smem = WarpSmem<M, KIND == 2>;
     static constexpr bool TM = PL::TM;
     Smem* sm;
-    WsHand* hs;      // ROLE 1/2: this frame slot's handoff
-    uint32_t par_;   // ROLE 1: parity of the next B phase; ROLE 2: of the next C phase
     float4* r0g;  // this warp's channel LLRs in global scratch, lane-private pass-0 layout (n < 1024)
     uint32_t tb;  // this warp's TMEM columns (n = 1024)
     const uint32_t* fzt;  // n = 1024: walk0's frozen-row field words, [F/32][lane] (shared by the CTA)
@@ -1458,15 +1438,6 @@ struct Dec {
                 if constexpr (S == PL::SL - 1) {
                     PBP_T1(ts, 1);
                     PBP_T0(tw0);
-                    // warp-specialised: walk0 needs the frontier after iteration
-                    // t-1's last-pass commits (bookkeeping warp); stages 0..4 of
-                    // this sweep never read what those commits change (L(6..10))
-                    if constexpr (ROLE == 1) {
-                        PBP_T0(twb);
-                        const bool go = it == 1 || ws_wait_b();
-                        PBP_T1(twb, 5);
-                        if (!go) return false;
-                    }
                     walk0();
                     PBP_T1(tw0, 2);
                     return true;
@@ -1495,21 +1466,7 @@ struct Dec {
     // the decided prefix [0, pin) taken from decided_u; returned as the
     // row-order word of this lane (lane < NW).
     __device__ __forceinline__ uint32_t u_words(int pin) {
-        uint32_t uq;
-        if constexpr (ROLE == 2) {
-            // R(m) of the sweep, stored by the sweep warp at C_RM (last-pass layout)
-            uq = 0u;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float v[8];
-                tm::ld8(tb + kCRM + 8 * c, v);
-                tm::wait_ld();
-#pragma unroll
-                for (int i = 0; i < 8; ++i) uq |= (__float_as_uint(v[i]) >> 31) << (8 * c + i);
-            }
-        } else {
-            uq = pack_all();
-        }
+        uint32_t uq = pack_all();
         uq &= ~FZ[Q - 1];
         if (pin > 0) {
             const int r0 = P * lane;
@@ -1661,263 +1618,6 @@ struct Dec {
 #ifdef PBP_PROF_SECTIONS
         if (lane == 0)
             for (int i = 0; i < 8; ++i) atomicAdd(&g_prof[i], prof[i]);
-#endif
-    }
-
-    // ---- warp-specialised n = 1024 csfg (bp_ws_kernel) ---------------------
-    // TMEM columns of R(m) after each sweep (C_LM0's: the sweep warp rebuilds
-    // L(m) from the frozen mask at every frame start instead)
-    static constexpr uint32_t kCRM = PL::C_LM0;
-    // named barriers 2 slot (C) and 2 slot + 1 (B): all 16 hardware barriers
-    // (bar 0 is free again after the prologue's __syncthreads; the epilogue
-    // uses a shared-memory count instead). One barrier cannot carry both
-    // directions: the sweep warp's arrive C(t) and its sync B(t) would
-    // complete one instance by themselves when the bookkeeping warp is late.
-    int bar_id_;
-#ifndef PBP_WS_MBAR
-    __device__ __forceinline__ void ws_arrive(unsigned long long* b) { nb::arrive(bar_id_ + (b == &hs->mbB)); }
-    __device__ __forceinline__ void ws_sync_on(unsigned long long* b) { nb::sync(bar_id_ + (b == &hs->mbB)); }
-#else
-    __device__ __forceinline__ void ws_arrive(unsigned long long* b) { mb::arrive(b); }
-    __device__ __forceinline__ void ws_sync_on(unsigned long long* b) {
-        mb::wait(b, par_);
-        par_ ^= 1u;
-    }
-#endif
-    __device__ __forceinline__ void ws_sync() { ws_sync_on(&hs->mbB); }
-
-    // sweep warp: wait for the bookkeeping of iteration it-1; false when the
-    // frame ended there (this speculative sweep is dropped)
-    __device__ __forceinline__ bool ws_wait_b() {
-        ws_sync();
-        tm::fence_after();  // its L(m) column update (apply_tm) before our stage m-1 load
-        if (hs->bdone) return false;
-        frontier = hs->bfrontier;
-        return true;
-    }
-
-    // Sweep warp (ROLE 1): frames from the queue; per iteration t the stages
-    // (first pass, wait for iteration t-1's bookkeeping, walk0, last pass),
-    // then R(m) / x_hat / walk0's result to the bookkeeping warp, the
-    // first-pass commits' side effects (apply_early_tm, rare) and the register
-    // fix-up; then the next sweep starts at once (speculatively: the
-    // bookkeeping warp may find at B(t) that the frame ended with t).
-    __device__ __forceinline__ void run_sweep(const DecodeArgs& args, Smem* s, int ln) {
-        static_assert(TM && KIND == 2, "warp-specialised path: n = 1024 csfg");
-        a = &args;
-        sm = s;
-        lane = ln;
-        alpha = args.alpha;
-        par_ = 0u;
-        fz_init<0>();
-        if (lane < NW) sm->frz[lane] = a->frozen_bits[lane];
-        __syncwarp();
-        for (;;) {
-            long long f = 0;
-            if (lane == 0) f = (long long)atomicAdd(args.queue, 1ull);
-            f = __shfl_sync(kFull, f, 0);
-            if (f >= args.frames) {
-                if (lane == 0) hs->frame = -1;
-                __syncwarp();
-                ws_arrive(&hs->mbC);
-                break;
-            }
-            frame_ = f;
-            if (!load_frame(f)) {
-                if (lane == 0) {
-                    const unsigned long long slot = atomicAdd(args.list_len, 1ull);
-                    args.list[slot] = f + args.frame_base;
-                }
-                continue;
-            }
-            // init_frame without TMEM's pristine L(m) copy: L(m) = +CAP at frozen
-            // rows from the mask (an opaque copy per frame: not hoisted)
-            {
-                uint32_t fl;
-                asm volatile("mov.b32 %0, %1;" : "=r"(fl) : "r"(FZ[Q - 1]));
-#pragma unroll
-                for (int j = 0; j < P; ++j) R[j] = ((fl >> j) & 1u) ? kCap : 0.f;
-                tm::st_row<kTG>(tb + PL::C_LM, R);
-            }
-            init_smem_ws();
-#pragma unroll
-            for (int j = 0; j < P; ++j) R[j] = 0.f;
-#pragma unroll
-            for (int sl = 0; sl < PL::NLR; ++sl)
-#pragma unroll
-                for (int j = 0; j < P; ++j) Lr[sl][j] = 0.f;
-            frontier = 0;
-            prot = 0u;
-            xq = 0u;
-            tm::wait_st();
-            if (args.max_iter < 1) {  // no sweep: the bookkeeping warp writes the outputs
-                if (lane == 0) {
-                    hs->frame = (int)f;
-                    hs->it = 0;
-                }
-                __syncwarp();
-                ws_arrive(&hs->mbC);
-                ws_wait_b();
-                continue;
-            }
-            PBP_T0(tl);
-#pragma unroll 1
-            for (int t = 1;; ++t) {
-                it = t;
-                if (!sweep_from<0>()) break;  // B(t-1) said the frame ended at t-1
-                PBP_T0(tx);
-                tm::st_row<kTG>(tb + kCRM, R);  // R(m) for the G-check / outputs
-                hs->xq[lane] = xq;
-                const int dinact = nce_ ? apply_early_tm() : 0;
-                if (lane < 16) hs->dinact[lane] = lane < M ? dinact : 0;
-                if (lane == 0) {
-                    hs->frame = (int)f;
-                    hs->it = t;
-                    hs->nce = nce_;
-                    hs->s_last = s_last_;
-                    hs->done = done_ ? 1 : 0;
-                    hs->frontier = frontier;
-                    hs->L1 = L1;
-                    hs->fr_start = fr_start_;
-                }
-                tm::wait_st();
-                tm::fence_before();
-                __syncwarp();
-                ws_arrive(&hs->mbC);
-                if (prot & ((1u << PL::NLR) - 1u)) fixup_regs();
-                PBP_T1(tx, 4);
-                if (done_ || t >= args.max_iter) {  // the frame ends with this iteration
-                    PBP_T0(twb);
-                    ws_wait_b();
-                    PBP_T1(twb, 5);
-                    break;
-                }
-            }
-            PBP_T1(tl, 7);
-        }
-#ifdef PBP_PROF_SECTIONS
-        if (lane == 0)
-            for (int i = 0; i < 8; ++i) atomicAdd(&g_prof[i], prof[i]);
-#endif
-    }
-
-    // init_smem for the sweep warp (L(m) is set by run_sweep; dec_u / fst are
-    // free: the bookkeeping warp finished the previous frame before B)
-    __device__ __forceinline__ void init_smem_ws() {
-#pragma unroll 1
-        for (int sl = 0; sl < PL::NLS; ++sl)
-#pragma unroll 1
-            for (int c = 0; c < P / 4; ++c) sm->Ls[sl][c][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 1
-        for (int i = lane; i < PL::NX; i += 32) sm->X[0][i] = 0.f;
-        if (lane < NW) sm->dec_u[lane] = 0u;
-        if (lane < NW) sm->xprot[0][lane] = 0u;
-#pragma unroll 1
-        for (int sl = 0; sl < PL::NLR + PL::NLS; ++sl) sm->pm[sl][lane] = 0u;
-#pragma unroll 1
-        for (int i = lane; i < N / 4; i += 32) reinterpret_cast<uint32_t*>(sm->fst)[i] = 0x7f7f7f7fu;
-        __syncwarp();
-    }
-
-    // Bookkeeping warp (ROLE 2): for every exported sweep the reference's
-    // stage loop over the last pass (walk_tm), apply_freeze of its commits
-    // (apply_tm), the PE count, the pinned G-check and, when the frame ends,
-    // its outputs and counters; then B.
-    __device__ __forceinline__ void run_bk(const DecodeArgs& args, Smem* s, int ln) {
-        static_assert(TM && KIND == 2, "warp-specialised path: n = 1024 csfg");
-        a = &args;
-        sm = s;
-        lane = ln;
-        par_ = 0u;
-        {
-            uint32_t w = 0u;
-#pragma unroll 1
-            for (int j = 0; j < P; ++j) w |= (uint32_t)(a->frozen_rows[row_of<Q - 1>(j)] != 0) << j;
-            FZ[Q - 1] = w;
-        }
-        {
-            const int j = lane;
-            constexpr int d = P / 2;
-            const int hi = (j >= d) ? 1 : 0;
-            const int jj = j - hi * d;
-            xperm = P - 1 - (4 * (jj >> 1) + 2 * hi + (jj & 1));
-        }
-        if (lane < kNumCounters) sm->cnt[lane] = 0ull;
-        cset_ = 0;
-        __syncwarp();
-#ifdef PBP_PROF_SECTIONS
-        const long long tstart = clock64();
-#endif
-        for (;;) {
-            PBP_T0(twc);
-            ws_sync_on(&hs->mbC);
-            tm::fence_after();
-            PBP_T1(twc, 0);
-            const int f = hs->frame;
-            if (f < 0) break;
-            const int t = hs->it;
-            frame_ = f;
-            it = t;
-            if (t <= 1) {
-                frontier = 0;
-                inact = 0;
-                nev = 0;
-                act = 0;
-            }
-            bool finished = true;
-            int stop = 0;
-            uint32_t uw = 0u;
-#ifdef PBP_WS_NULLBK
-            if (t > 0) {  // timing experiment only: no bookkeeping (wrong results)
-                finished = hs->done || t >= args.max_iter;
-            } else
-#endif
-            if (t > 0) {
-                nce_ = hs->nce;
-                s_last_ = hs->s_last;
-                done_ = hs->done != 0;
-                frontier = hs->frontier;
-                L1 = hs->L1;
-                fr_start_ = hs->fr_start;
-                xq = hs->xq[lane];
-                int dinact = lane < 16 ? hs->dinact[lane] : 0;
-                nev += nce_;
-                PBP_T0(tw);
-                LateTM w;
-                walk_tm(w);
-                PBP_T1(tw, 1);
-                PBP_T0(ta);
-                if (w.cm) apply_tm(w, dinact);
-                if (lane < M) inact += dinact;
-                const int v = lane <= s_last_ ? (N >> 1) - inact : 0;
-                act += __reduce_add_sync(kFull, v);
-                PBP_T1(ta, 2);
-                PBP_T0(tg);
-                bool converged = false;
-                if (!done_) converged = gcheck(frontier);
-                PBP_T1(tg, 3);
-                finished = done_ || converged || t >= args.max_iter;
-                if (finished) {
-                    stop = frontier >= N ? 2 : (converged ? 1 : 0);
-                    uw = frontier >= N ? (lane < NW ? sm->dec_u[lane] : 0u) : u_words(frontier);
-                }
-            }
-            if (finished) write_outputs(f, uw, t, stop);
-            if (lane == 0) {
-                hs->bdone = finished ? 1 : 0;
-                hs->bfrontier = frontier;
-            }
-            tm::wait_st();  // apply_tm's L(m) column
-            tm::fence_before();
-            __syncwarp();
-            ws_arrive(&hs->mbB);
-        }
-        if (args.counters && lane < kNumCounters && sm->cnt[lane])
-            atomicAdd(&args.counters[cset_ * kNumCounters + lane], sm->cnt[lane]);
-#ifdef PBP_PROF_SECTIONS
-        prof[7] = clock64() - tstart;
-        if (lane == 0)
-            for (int i = 0; i < 8; ++i) atomicAdd(&g_prof[8 + i], prof[i]);
 #endif
     }
 
@@ -2120,86 +1820,7 @@ __global__ void __launch_bounds__(32 * Plan<M>::WARPS, Plan<M>::TM ? 1 : kMinWar
     }
 }
 
-// n = 1024 csfg, warp-specialised: 16 warps per CTA, one CTA per SM. Warps
-// 0..7 are the sweep warps of frame slots 0..7 (registers raised to 224 with
-// setmaxnreg), warps 8..15 their bookkeeping warps (lowered to 32); slot i's
-// two warps share one lane quarter of TMEM (warp % 4) and slot i's 256 columns.
-#ifndef PBP_WS_BK_REGS
-#define PBP_WS_BK_REGS 32
-#endif
-constexpr int kWsBkRegs = PBP_WS_BK_REGS, kWsSweepRegs = 256 - kWsBkRegs;
-template <int M, int KIND>
-__global__ void __launch_bounds__(512, 1) bp_ws_kernel(DecodeArgs a) {
-    static_assert(Plan<M>::TM && KIND == 2 && Plan<M>::WARPS == 8, "n = 1024 csfg");
-    extern __shared__ __align__(16) unsigned char wsm[];
-    using Smem = typename Dec<M, KIND>::Smem;
-    __shared__ uint32_t tbase;
-    __shared__ unsigned ws_done;
-    const int warp = threadIdx.x >> 5, slot = warp & 7;
-    if (threadIdx.x == 0) ws_done = 0u;
-    Smem* slots = reinterpret_cast<Smem*>(wsm);
-    uint32_t* fzt = reinterpret_cast<uint32_t*>(slots + 8);
-    WsHand* hand = reinterpret_cast<WsHand*>(fzt + 32 * 32);
-    if (warp == 0) tm::alloc512(&tbase);
-    // walk0's frozen-row fields for every frontier word (as bp_warp_kernel)
-    for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
-        const int jf = i >> 5, ln = i & 31;
-        uint32_t fz0 = 0u;
-        for (int j = 0; j < 32; ++j) fz0 |= (uint32_t)(a.frozen_rows[ln + 32 * j] != 0) << j;
-        fzt[i] = ((fz0 >> (jf & ~15)) & 0xFFFFu) | (((fz0 >> (jf & ~7)) & 0xFFu) << 16) |
-                 (((fz0 >> (jf & ~3)) & 0xFu) << 24) | (((fz0 >> (jf & ~1)) & 3u) << 28) | (((fz0 >> jf) & 1u) << 30);
-    }
-    if (threadIdx.x < 8) {
-        mb::init(&hand[threadIdx.x].mbC, 32);
-        mb::init(&hand[threadIdx.x].mbB, 32);
-    }
-    tm::fence_before();
-    __syncthreads();
-    tm::fence_after();
-    if (warp < 8) {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsSweepRegs));
-        Dec<M, KIND, false, 1> dec;
-        dec.tb = tm::warp_base(tbase, slot);
-        dec.fzt = fzt;
-        dec.hs = hand + slot;
-        dec.bar_id_ = 2 * slot;
-        dec.run_sweep(a, slots + slot, threadIdx.x & 31);
-    } else {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsBkRegs));
-        Dec<M, KIND, false, 2> dec;
-        dec.tb = tm::warp_base(tbase, slot);
-        dec.fzt = fzt;
-        dec.hs = hand + slot;
-        dec.bar_id_ = 2 * slot;
-        dec.run_bk(a, slots + slot, threadIdx.x & 31);
-    }
-    // epilogue: every warp done with TMEM before warp 0 frees it (a count, not
-    // bar 0, which slot 0's handoff may still be using)
-    tm::fence_before();
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) atomicAdd(&ws_done, 1u);
-    if (warp == 0) {
-        while (atomicAdd(&ws_done, 0u) < 16u) __nanosleep(256);
-        tm::fence_after();
-        tm::dealloc512(tbase);
-    }
-}
-
-template <int M, int KIND>
-constexpr size_t ws_smem() {
-    return 8 * sizeof(typename Dec<M, KIND>::Smem) + 32 * 32 * sizeof(uint32_t) + 8 * sizeof(WsHand);
-}
-
 }  // namespace wk
-
-// PBP_WS=0 selects the one-warp-per-frame kernel for n = 1024 csfg (A/B runs)
-static bool ws_enabled() {
-    static const int v = [] {
-        const char* e = getenv("PBP_WS");
-        return (e && e[0] == '0') ? 0 : 1;
-    }();
-    return v != 0;
-}
 
 int warp_kernel_supported(int m) { return m >= 7 && m <= 10; }
 // warps (frames) per CTA of the warp kernel: eight at n = 1024 (TMEM), else one
@@ -2231,16 +1852,6 @@ template <int M, int KIND>
 static cudaError_t launch_w(const DecodeArgs& a, int grid, cudaStream_t st) {
     if constexpr (KIND == 2) {
         if (a.ev_xhat) return launch_wx<M, KIND, true>(a, grid, st);  // trace with x_hat
-        if constexpr (wk::Plan<M>::TM) {
-            if (!a.events && ws_enabled()) {  // event lists: the one-warp kernel records them
-                constexpr size_t smem = wk::ws_smem<M, KIND>();
-                cudaError_t e = cudaFuncSetAttribute(wk::bp_ws_kernel<M, KIND>,
-                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                if (e != cudaSuccess) return e;
-                wk::bp_ws_kernel<M, KIND><<<grid, 512, smem, st>>>(a);
-                return cudaGetLastError();
-            }
-        }
     }
     return launch_wx<M, KIND, false>(a, grid, st);
 }

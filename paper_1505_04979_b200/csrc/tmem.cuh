@@ -128,42 +128,4 @@ __device__ __forceinline__ void ld1(uint32_t a, float* v) {
 }
 
 }  // namespace tm
-
-// mbarriers in shared memory: the per-frame handoff between the sweep warp and
-// the bookkeeping warp of the warp-specialised n = 1024 decoder. Every lane
-// of the producing warp arrives (count 32, release), every lane of the
-// consumer waits on the phase parity (acquire).
-namespace mb {
-__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void init(unsigned long long* b, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void arrive(unsigned long long* b) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
-}
-// a wait that never completes (a protocol bug) traps after ~10 s instead of
-// hanging the device
-__device__ __forceinline__ void wait(unsigned long long* b, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok) : "r"(sa(b)), "r"(parity) : "memory");
-    if (ok) return;
-    const long long t0 = clock64();
-    do {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(ok) : "r"(sa(b)), "r"(parity) : "memory");
-        if (!ok && clock64() - t0 > 20000000000ll) __trap();
-    } while (!ok);
-}
-}  // namespace mb
-
-// named hardware barriers for the same handoff: the waiting warp sleeps in the
-// barrier instead of polling (arrive: release, sync: acquire among the 64
-// participating threads)
-namespace nb {
-__device__ __forceinline__ void arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
-__device__ __forceinline__ void sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
-}  // namespace nb
 }  // namespace pbp
