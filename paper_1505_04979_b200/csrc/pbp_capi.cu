@@ -322,7 +322,8 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
         a.queue = s.ctl.p + 0;
         a.list_mode = 0;
         const int per_sm = warp_occupancy(ctx, r.kind);
-        const long long grid = std::min<long long>((long long)per_sm * ctx->sm_count, r.frames);
+        long long grid = std::min<long long>((long long)per_sm * ctx->sm_count, r.frames);
+        if (const char* gc = getenv("PBP_GRID_CAP")) grid = std::max(1ll, std::min(grid, atoll(gc)));  // experiments
         cudaError_t e;
         if (fk == 1) {
             a.r0s = s.r0s.p;
