@@ -135,6 +135,7 @@ struct alignas(16) WarpSmem {
     uint32_t frz[PL::NW];                  // frozen rows, row-order words
     uint32_t fz[PL::Q][32];                // frozen rows per pass layout
     uint8_t fst[PL::N];                    // freeze_stage per row
+    uint32_t skipm[PL::TM ? 5 : 1];        // PBP_SKIP_FROZEN: pass-0 register columns inactive at stage s
 };
 
 __device__ __forceinline__ float xsmin(float a, float b) {
@@ -390,6 +391,18 @@ struct Dec {
 #else
         constexpr bool packed = true;
 #endif
+#ifdef PBP_SKIP_FROZEN
+        // experiment (DESIGN.md §5 "Skipping frozen PEs"): at n = 1024 a block frozen at
+        // stage f <= 3 covers whole register columns of the pass-0 layout (all 32
+        // lanes), so its PEs of stages f+1..4 are skipped by a warp-uniform branch per
+        // packed pair; the skipped rows keep stale R / L, which only inactive PEs and
+        // pinned rows read (the boundary L(f+1) is restored by fixup_regs as before)
+        constexpr bool kSkip = TM && KIND == 2 && q == 0 && S > 0;
+        const uint32_t skc = kSkip ? sm->skipm[S] : 0u;
+#else
+        constexpr bool kSkip = false;
+        const uint32_t skc = 0u;
+#endif
         if constexpr (d >= 2 && packed) {
             // stage 0: x_hat bits pushed into four independent 8-bit chains
             // (pushes 8c..8c+7 in chain c), concatenated below into the same bit
@@ -398,6 +411,7 @@ struct Dec {
 #pragma unroll
             for (int j = 0; j < P; j += 2) {
                 if (j & d) continue;
+                if (kSkip && ((skc >> j) & 3u) == 3u) continue;  // warp-uniform
                 const float lt0 = Lt[j], lt1 = Lt[j + 1], lb0 = Lt[j + d], lb1 = Lt[j + d + 1];
                 const float rt0 = R[j], rt1 = R[j + 1], rb0 = R[j + d], rb1 = R[j + d + 1];
                 float c0, c1, s0, s1, lt0o, lt1o, rt0o, rt1o, lb0o, lb1o, rb0o, rb1o;
@@ -444,6 +458,7 @@ struct Dec {
 #pragma unroll
             for (int j = 0; j < P; ++j) {
                 if (j & d) continue;
+                if (kSkip && ((skc >> j) & 1u)) continue;  // warp-uniform
                 const float lt = Lt[j], lb = Lt[j + d], rt = R[j], rb = R[j + d];
                 const float cross = __fmul_rn(alpha, xsmin(lt, rt));
                 const float sum_bot = __fadd_rn(lb, rb);
@@ -986,6 +1001,12 @@ struct Dec {
             //    those already inactive at s2 are counted once (packed warp sums)
             if (lane > S && lane < M) dinact += sz >> 1;
             if (k == 0 && start < fr_start) dinact -= recovered_inactive(S, start, fr_start);
+#ifdef PBP_SKIP_FROZEN
+            if (S <= 3 && lane == 0) {  // register columns start/32 .. (start+sz)/32 - 1
+                const uint32_t cols = low_mask(sz >> 5) << ((start >> 5) & 31);
+                for (int s2 = S + 1; s2 <= 4; ++s2) sm->skipm[s2] |= cols;
+            }
+#endif
             //    freeze_stage over the block (:86), 16 bytes per lane and step
             {
                 const uint32_t w4 = 0x01010101u * (uint32_t)S;
@@ -1760,6 +1781,7 @@ struct Dec {
                                               ((fl >> (4 * c + 3)) & 1u) ? kCap : 0.f);
         }
         if (lane < NW) sm->dec_u[lane] = 0u;
+        if (TM && lane < 5) sm->skipm[lane] = 0u;
 #pragma unroll 1
         for (int x = 0; x < Q - 1; ++x)
             if (lane < NW) sm->xprot[x][lane] = 0u;
