@@ -1055,12 +1055,11 @@ struct Dec {
         uint32_t xb = 0u;
         int tr = 0;
 #pragma unroll
-        for (int t = 0; t < 5; ++t) {
-            if (((cm >> t) & 1u) && (unsigned)(r - w.At[t]) < (16u >> t)) {
-                Sr = 5 + t;
-                tr = t;
-                xb = (w.x[t] >> lane) & 1u;
-            }
+        for (int t = 0; t < 5; ++t) {  // selects: the committed blocks are disjoint
+            const bool in = ((cm >> t) & 1u) && (unsigned)(r - w.At[t]) < (16u >> t);
+            Sr = in ? 5 + t : Sr;
+            tr = in ? t : tr;
+            xb = in ? (w.x[t] >> lane) & 1u : xb;
         }
         const uint32_t ub = (__shfl_sync(kFull, w.u, tr) >> lane) & 1u;
         const bool cov = Sr >= 0;
@@ -1081,13 +1080,12 @@ struct Dec {
                 if (lane >= 6 && lane < M) dinact -= (int)((c >> (8 * (lane - 6))) & 0xffu);
             }
         }
-        if (cov) {
+        {  // predicated stores (no divergent branch): L(S+1) saturation and freeze_stage of row r
             const int owner = r >> 5, j = r & 31;
-            if (Sr < M - 1) {
-                float* base = reinterpret_cast<float*>(&sm->Ls[Sr - 5][0][0]);
-                base[((j >> 2) * 32 + owner) * 4 + (j & 3)] = xb ? -kCap : kCap;
-            }
-            sm->fst[r] = (uint8_t)Sr;
+            float* base = reinterpret_cast<float*>(&sm->Ls[(Sr > 5 ? Sr : 5) - 5][0][0]);
+            const float sv = __uint_as_float(__float_as_uint(kCap) | (xb << 31));
+            if (cov && Sr < M - 1) base[((j >> 2) * 32 + owner) * 4 + (j & 3)] = sv;
+            if (cov) sm->fst[r] = (uint8_t)Sr;
         }
         if (c9) {  // stage m-1: L(m) of one row, TMEM column j of lane owner
             const int r9 = w.At[4];
@@ -1098,14 +1096,11 @@ struct Dec {
         }
         // decided_u over the window (two row-order words; shared atomics: no round trip)
         const uint32_t cvw = __ballot_sync(kFull, cov), uw = __ballot_sync(kFull, cov && ub);
-        if (lane < 2) {
+        {  // lanes 0 and 1 own the window's two words: plain read-modify-write
             const int wd = (A5 >> 5) + lane, sh = A5 & 31;
             const uint32_t mk = lane == 0 ? cvw << sh : (sh ? cvw >> (32 - sh) : 0u);
             const uint32_t vv = lane == 0 ? uw << sh : (sh ? uw >> (32 - sh) : 0u);
-            if (mk) {
-                atomicAnd(&sm->dec_u[wd], ~mk);
-                atomicOr(&sm->dec_u[wd], vv);
-            }
+            if (lane < 2 && mk) sm->dec_u[wd] = (sm->dec_u[wd] & ~mk) | vv;
         }
         // inactive top rows: a stage-S block of B rows has B/2 top rows at every later stage
         if (lane < M) dinact += (int)((__brev((cm << 5) & ((1u << lane) - 1u)) >> (32 - M)) >> 1);
