@@ -177,6 +177,19 @@ __device__ __forceinline__ uint32_t jmask(int tp) {
          : tp == 3 ? 0x00FF00FFu : 0x0000FFFFu;
 }
 
+#ifdef PBP_DEBUG_PROGRESS
+// hang debugging only: per-warp progress words in mapped host memory
+__device__ unsigned long long* g_dbg;
+extern "C" int pbp_debug_set(void* p) { return cudaMemcpyToSymbol(g_dbg, &p, sizeof(p)) != cudaSuccess; }
+#define PBP_DBG(loc)                                                                                           \
+    do {                                                                                                       \
+        if (lane == 0 && g_dbg)                                                                                \
+            *(volatile unsigned long long*)&g_dbg[blockIdx.x * 8 + (threadIdx.x >> 5)] =                       \
+                ((unsigned long long)frame_ << 32) | ((unsigned long long)it << 8) | (unsigned long long)(loc); \
+    } while (0)
+#else
+#define PBP_DBG(loc)
+#endif
 #ifdef PBP_PROF_SECTIONS
 // timing experiments only: per-warp clock64 time per code section
 __device__ unsigned long long g_prof[8];
@@ -665,7 +678,9 @@ struct Dec {
     // 3 dB). Commit side effects follow after the sweep (apply_commits).
     __device__ __forceinline__ void walk0() {
         static_assert(M == 10 && PL::SL == 5 && P == 32, "walk0: n = 1024 layout");
+        PBP_DBG(10);
         tm::wait_st();  // this sweep's snapshots
+        PBP_DBG(11);
         fr_start_ = frontier;
         int nc = 0;
         s_last_ = M - 1;
@@ -714,6 +729,7 @@ struct Dec {
                 if (!((lane >> gp) & 1)) u ^= o;
             }
             const uint32_t fzw = fzt[jf * 32 + lane];  // frozen rows of the five blocks, same fields
+            PBP_DBG(12);
             const uint32_t V = __reduce_or_sync(kFull, u & fzw);
             uint32_t acc = (uint32_t)((V & 0xFFFFu) == 0u) | ((uint32_t)(((V >> 16) & 0xFFu) == 0u) << 1) |
                            ((uint32_t)(((V >> 24) & 0xFu) == 0u) << 2) | ((uint32_t)(((V >> 28) & 3u) == 0u) << 3) |
@@ -742,6 +758,7 @@ struct Dec {
         }
         nce_ = nc;
         L1 = done_ ? -4 : frontier / P;
+        PBP_DBG(13);
     }
 
     // last-pass stage S: lanes L1 and L1+1 keep R(S+1) (rows P*lane + j)
@@ -1481,8 +1498,28 @@ struct Dec {
     // û in the last-pass layout (rows P*lane + j), frozen rows forced to 0,
     // the decided prefix [0, pin) taken from decided_u; returned as the
     // row-order word of this lane (lane < NW).
-    __device__ __forceinline__ uint32_t u_words(int pin) {
-        uint32_t uq = pack_all();
+    // TM csfg: R(m) of the last finished sweep, kept for the G-check and the
+    // outputs while the next sweep's stage 0 runs (stage 4's snapshot columns:
+    // walk0 has read them, stage 4 of the next sweep rewrites them)
+    static constexpr uint32_t C_SAVE = PL::C_S + 128;
+    __device__ __forceinline__ uint32_t signs_saved() const {
+        tm::wait_st();  // the sweep's R(m) store
+        uint32_t uq = 0u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            float v[8];
+            tm::ld8(tb + C_SAVE + 8 * c, v);
+            tm::wait_ld();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) uq |= (__float_as_uint(v[i]) >> 31) << (8 * c + i);
+        }
+        return uq;
+    }
+
+    __device__ __forceinline__ uint32_t u_words(int pin, bool saved = false) {
+        uint32_t uq;
+        if constexpr (TM) uq = saved ? signs_saved() : pack_all();
+        else uq = pack_all();
         uq &= ~FZ[Q - 1];
         if (pin > 0) {
             const int r0 = P * lane;
@@ -1525,16 +1562,108 @@ struct Dec {
         return gcheck_full(pin);
     }
 
-    __device__ __forceinline__ bool gcheck_full(int pin) {
-        uint32_t uw = u_words(pin);
+    __device__ __forceinline__ bool gcheck_full(int pin, bool saved = false, uint32_t xqv = 0u) {
+        uint32_t uw = u_words(pin, saved);
         uw = word_transform(uw, 32);
 #pragma unroll
         for (int h = 1; h < NW; h <<= 1) {
             const uint32_t o = __shfl_xor_sync(kFull, uw, h);
             if (!(lane & h)) uw ^= o;
         }
-        const uint32_t xw = __shfl_sync(kFull, transpose32(xq, lane), xperm);
+        const uint32_t xw = __shfl_sync(kFull, transpose32(saved ? xqv : xq, lane), xperm);
         return !__any_sync(kFull, lane < NW && uw != xw);
+    }
+
+    // gcheck's exact filter without a branch: false proves x_hat != G(u_hat')
+    __device__ __forceinline__ bool gfilter(int pin, uint32_t xqv) {
+        const uint32_t free0 = ~sm->frz[0] & ~low_mask(pin < 32 ? pin : 32);
+        const uint32_t cls = __ballot_sync(kFull, __popc(xqv) & 1);
+        const uint32_t u0 = pin > 0 ? sm->dec_u[0] & low_mask(pin < 32 ? pin : 32) : 0u;
+        return free0 != 0u || cls == word_transform(u0, 32);
+    }
+
+    // the last-pass commits and the PE count of the sweep that ended (a no-op
+    // when cm = 0 and !live): run inside the next sweep's stage 0
+    __device__ __forceinline__ void book_tail(const LateTM& w, int dinact, bool live) {
+        apply_tm(w, dinact);
+        if (lane < M) inact += dinact;
+        const int v = (live && lane <= s_last_) ? (N >> 1) - inact : 0;
+        act += __reduce_add_sync(kFull, v);
+    }
+
+    // n = 1024 csfg decode of one frame, software-pipelined: after sweep t the
+    // last-pass walk, the first-pass commits and the register fix-up run at
+    // once (sweep t+1's stages read their results); apply_freeze of the
+    // last-pass commits, the PE count and the G-check filter of sweep t run in
+    // the same straight-line block as sweep t+1's stage 0, which reads none of
+    // what they write (R(0), L(1) against L(6..10), freeze state, decided_u),
+    // so their latency chains hide under its PE math. When the G-check finds
+    // sweep t converged, the speculative stage 0 is dropped (R(m) and x_hat of
+    // sweep t are kept in TMEM / a register for the check and the outputs).
+    __device__ __forceinline__ void decode_tm_csfg(int& iters, int& stop, uint32_t& uw) {
+        const DecodeArgs& args = *a;
+        iters = 0;
+        bool converged = false, pend = false;
+        // the first book_tail (nothing pending) reads the walk state before any walk0
+        // has set it: uniform values, or the warp's collectives would diverge on
+        // uninitialised registers
+        nce_ = 0;
+        fr_start_ = 0;
+        s_last_ = -1;
+        done_ = false;
+        LateTM w;
+        w.cm = 0u;
+        w.A5 = 0;
+        w.u = 0u;
+        w.xl = 0u;
+        w.Al = 0;
+#pragma unroll
+        for (int t = 0; t < PL::NL; ++t) {
+            w.x[t] = 0u;
+            w.At[t] = 0;
+        }
+        int dpend = 0;
+        uint32_t xqp = 0u;
+#pragma unroll 1
+        for (int t = 1; t <= args.max_iter; ++t) {
+            it = t - 1;  // events of the pending commits carry their own iteration
+            PBP_DBG(1);
+            book_tail(w, dpend, pend);
+            const bool full = pend && gfilter(frontier, xqp);
+            it = t;
+            PBP_DBG(2);
+            stage<0>();
+            PBP_DBG(3);
+            if (pend) {
+                pend = false;
+                if (full) converged = gcheck_full(frontier, true, xqp);
+                if (converged) break;  // the frame ended with sweep t-1
+            }
+            iters = t;
+            sweep_from<1>();
+            PBP_DBG(4);
+            tm::st_row<kTG>(tb + C_SAVE, R);  // R(m) of sweep t
+            xqp = xq;
+            walk_tm(w);
+            PBP_DBG(5);
+            dpend = nce_ ? apply_early_tm() : 0;
+            if (prot & ((1u << PL::NLR) - 1u)) fixup_regs();
+            __syncwarp();
+            pend = true;
+            if (done_) break;  // the frontier reached n: no G-check
+            w.cm = w.cm;  // keep w live across the loop edge
+        }
+        PBP_DBG(6);
+        if (pend) {  // the last sweep's commits and count; its G-check when the frontier is < n
+            it = iters;
+            book_tail(w, dpend, true);
+            if (!done_) converged = gfilter(frontier, xqp) && gcheck_full(frontier, true, xqp);
+        }
+        PBP_DBG(7);
+        stop = frontier >= N ? 2 : (converged ? 1 : 0);
+        if (frontier >= N) uw = lane < NW ? sm->dec_u[lane] : 0u;
+        else uw = u_words(frontier, iters > 0);
+        PBP_DBG(8);
     }
 
     __device__ __forceinline__ void run(const DecodeArgs& args, Smem* s, int ln) {
@@ -1588,6 +1717,15 @@ struct Dec {
             int iters = (KIND == 0) ? args.max_iter : 0;
             int stop = 0;
             bool converged = false;
+#ifndef PBP_NO_PIPELINE
+            if constexpr (TM && KIND == 2) {
+                uint32_t uwp;
+                decode_tm_csfg(iters, stop, uwp);
+                PBP_T1(tl, 7);
+                write_outputs(f, uwp, iters, stop);
+                continue;
+            }
+#endif
 #pragma unroll 1
             for (int t = 1; t <= args.max_iter; ++t) {
                 if constexpr (KIND == 2) {
