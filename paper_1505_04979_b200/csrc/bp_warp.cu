@@ -1600,6 +1600,11 @@ struct Dec {
     // so their latency chains hide under its PE math. When the G-check finds
     // sweep t converged, the speculative stage 0 is dropped (R(m) and x_hat of
     // sweep t are kept in TMEM / a register for the check and the outputs).
+#ifndef PBP_PIPE
+#define PBP_PIPE 1
+#endif
+    static constexpr int kPipe = PBP_PIPE;  // stages of the next sweep the book-keeping overlaps
+    static_assert(kPipe >= 1 && kPipe <= 4, "stages 0..3 only (walk0 runs at stage 4)");
     __device__ __forceinline__ void decode_tm_csfg(int& iters, int& stop, uint32_t& uw) {
         const DecodeArgs& args = *a;
         iters = 0;
@@ -1632,7 +1637,12 @@ struct Dec {
             const bool full = pend && gfilter(frontier, xqp);
             it = t;
             PBP_DBG(2);
+            // stages 0 .. kPipe-1 of sweep t read none of the pending book-keeping's
+            // results (only walk0, at stage 4, needs the new frontier)
             stage<0>();
+            if constexpr (kPipe > 1) stage<1>();
+            if constexpr (kPipe > 2) stage<2>();
+            if constexpr (kPipe > 3) stage<3>();
             PBP_DBG(3);
             if (pend) {
                 pend = false;
@@ -1640,7 +1650,7 @@ struct Dec {
                 if (converged) break;  // the frame ended with sweep t-1
             }
             iters = t;
-            sweep_from<1>();
+            sweep_from<kPipe>();
             PBP_DBG(4);
             tm::st_row<kTG>(tb + C_SAVE, R);  // R(m) of sweep t
             xqp = xq;
