@@ -44,6 +44,27 @@ def test_golden_case(ctx, golden, case, generic):
     _cmp(r, golden, name)
 
 
+@pytest.mark.timeout(600, method="thread")  # a hung kernel blocks the signal method
+def test_golden_cases_back_to_back(ctx, golden):
+    """Every golden case twice in a row on one context, fast and generic kernels
+    interleaved: each launch starts on the shared and tensor memory the previous
+    kernels left behind, so a read of uninitialised per-warp state (it once diverged
+    the n = 1024 kernel's collectives and hung it) shows up as a wrong result or a
+    timeout here."""
+    for _ in range(2):
+        for case in MAN["cases"]:
+            name = case["name"]
+            code = P.PolarCode.from_frozen_mask(case["n"], golden[name + "/frozen"])
+            for generic in (False, True):
+                ctx.force_generic(generic)
+                try:
+                    r = P.decode_batch(code, case["decoder"], golden[name + "/llr32"], 0.9375, case["max_iter"],
+                                       ctx=ctx)
+                finally:
+                    ctx.force_generic(False)
+                _cmp(r, golden, name)
+
+
 @pytest.mark.parametrize("generic", [False, True], ids=["auto", "generic"])
 def test_event_traces(ctx, golden, generic):
     ctx.force_generic(generic)
