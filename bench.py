@@ -171,13 +171,12 @@ def dram_traffic(frames_per_launch):
     bp_warp_kernel<10,2>, scaled per frame to this launch size); None if absent."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")))
-    if not files:
-        return None
-    try:
-        s = json.load(open(files[-1]))
-        return float(s["csfg"]["dram_bytes_per_frame"]) * frames_per_launch
-    except Exception:
-        return None
+    for f in reversed(files):  # the newest summary of the headline kernel (other kernels' summaries skipped)
+        try:
+            return float(json.load(open(f))["csfg"]["dram_bytes_per_frame"]) * frames_per_launch
+        except Exception:
+            continue
+    return None
 
 
 def cpu_model():
