@@ -106,6 +106,7 @@ SIGNATURES = {
                                                   C.POINTER(C.c_uint32), C.c_int64, C.c_int64, C.c_float,
                                                   C.c_int32, C.POINTER(C.c_int64), _P]),
     "pbp_kernel_path": (C.c_int, [C.c_int32]),
+    "pbp_kernel_cluster": (C.c_int, [C.c_int32, C.c_int]),
     "pbp_ctx_force_generic": (C.c_int, [_P, C.c_int]),
     "pbp_kernel_info": (C.c_int, [C.c_int32, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "pbp_last_launch_info": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),

@@ -35,6 +35,7 @@
 // clamp-free bound or non-finite are re-routed to the generic kernel, which
 // keeps every clamp.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "pbp_common.cuh"
@@ -50,7 +51,7 @@ enum : int { kReg = 0, kSmem = 1, kGlob = 2, kBits = 3, kTmem = 4 };
 
 // Per-size plan: threads (LOGT), rows per thread (2^K), where each L level
 // lives, whether R(0) stays in registers, whether Rx is double-buffered.
-template <int M>
+template <int M, bool SP = false>
 struct Cfg;
 template <>
 struct Cfg<11> {  // 128 threads x 16 rows, 3 CTAs per SM: four levels in registers, the rest in shared memory
@@ -94,9 +95,22 @@ struct Cfg<14> {  // 1024 x 16: one level in shared memory, four in TMEM, the re
     }
 };
 
-template <int M_>
+// SP (split pair): one CTA of a 2-CTA cluster holding half of a frame of
+// length 2^(M+1): its local stages 0..M-1 are the frame's stages 1..M, the
+// frame's stage 0 (distance 2^M) is the cross stage between the pair.
+template <>
+struct Cfg<13, true> {  // half of n = 16384: 512 x 16, one CTA per SM; inner levels 5..11 in TMEM, L(1) of the frame too
+    static constexpr int LOGT = 9, K = 4, MINB = 1;
+    static constexpr bool r0reg = false, rx2 = false;
+    static constexpr int TMEM_COLS = 512;  // 16 warps: 128 columns per warp = six levels + L(1) of the frame
+    static constexpr bool TPROT_REG = false;
+    static constexpr int where(int s) { return s == 13 ? kBits : (s <= 3) ? kReg : (s % 4 == 0) ? kSmem : kTmem; }
+};
+
+template <int M_, bool SP_ = false>
 struct Plan {
-    using C = Cfg<M_>;
+    using C = Cfg<M_, SP_>;
+    static constexpr bool SP = SP_;
     static constexpr int M = M_;
     static constexpr int N = 1 << M;
     static constexpr int LOGT = C::LOGT;
@@ -123,10 +137,12 @@ struct Plan {
     static constexpr int NTM = count(kTmem, M + 1);
     // TMEM: each warp owns TMEM_COLS * 4 / NWARP columns of its lane quarter, P per level
     static constexpr int TM_WCOLS = C::TMEM_COLS > 0 ? C::TMEM_COLS * 4 / NWARP : 0;
+    // SP: the frame's L(1) (local L(0), thread-private in pass 0's layout) in TMEM slot NTM
+    static constexpr int L0S = NTM;
     static constexpr bool tm_ok() {
         for (int s = 1; s <= M; ++s)
             if (C::where(s) == kTmem && !(s < M && s / K == (s - 1) / K)) return false;  // inner levels only
-        return NTM * P <= TM_WCOLS || NTM == 0;
+        return (NTM + (SP ? 1 : 0)) * P <= TM_WCOLS || (NTM == 0 && !SP);
     }
     static_assert(tm_ok(), "TMEM levels: thread-private (inner) levels that fit the warp's columns");
     static constexpr int pad(int row) { return row + (row >> 5); }
@@ -142,6 +158,45 @@ __device__ __forceinline__ float xsmin(float a, float b) {
     return d;
 }
 
+// thread-block cluster (SP pair): rank, barrier, distributed shared memory
+__device__ __forceinline__ int cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return (int)r;
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync() {
+    cluster_arrive();
+    cluster_wait();
+}
+// cluster window address of the same shared-memory object in CTA `rank`
+__device__ __forceinline__ uint32_t cluster_map(const void* p, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_peer(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_peer(uint32_t addr, int v) {
+    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_peer(uint32_t addr, float v) {
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_peer(uint32_t addr, long long v) {
+    asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_peer(uint32_t addr, unsigned long long v) {
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+
 // bit i (i & h == 0) absorbs bit i + h for h < 2^NB: the in-thread levels of
 // the polar transform (polar_code.cpp:13-20) over a thread's register rows
 template <int NB>
@@ -153,16 +208,17 @@ __device__ __forceinline__ uint32_t bits_transform(uint32_t w) {
     return w;
 }
 
-template <int M, typename = void>
+template <class C, typename = void>
 struct TprotReg { static constexpr bool value = false; };
-template <int M>
-struct TprotReg<M, std::void_t<decltype(Cfg<M>::TPROT_REG)>> { static constexpr bool value = Cfg<M>::TPROT_REG; };
+template <class C>
+struct TprotReg<C, std::void_t<decltype(C::TPROT_REG)>> { static constexpr bool value = C::TPROT_REG; };
 
-template <int M>
+template <int M, bool SP = false>
 struct Smem {
-    using PL = Plan<M>;
+    using PL = Plan<M, SP>;
+    using C = Cfg<M, SP>;
     float Ls[PL::NSM > 0 ? PL::NSM : 1][PL::NX];  // shared-memory L levels, row-indexed (padded)
-    float Rx[Cfg<M>::rx2 ? 2 : 1][PL::NX];         // R at pass boundaries
+    float Rx[C::rx2 ? 2 : 1][PL::NX];         // R at pass boundaries
     typename std::conditional<(PL::Q * PL::P > 32), unsigned long long, uint32_t>::type buf[PL::T];  // cross-warp words
     uint32_t vw[3];                                // verdict words of the pass checks
     uint32_t dec[PL::NW];                          // decided_u
@@ -171,24 +227,33 @@ struct Smem {
     long long frame;
     // TMEM levels: per thread and level, rows whose L is a frozen-block boundary
     // (bits 0..P-1) and their signs (bits 16..16+P-1), restored after each sweep
-    uint32_t tprot[(PL::NTM > 0 && !TprotReg<M>::value) ? PL::NTM : 1][(PL::NTM > 0 && !TprotReg<M>::value) ? PL::T : 1];
+    uint32_t tprot[(PL::NTM > 0 && !TprotReg<C>::value) ? PL::NTM : 1][(PL::NTM > 0 && !TprotReg<C>::value) ? PL::T : 1];
     uint32_t tbase;                                // TMEM allocation
+    // SP: what the peer CTA of the pair writes here (st.shared::cluster)
+    float mb[SP ? PL::P : 1][SP ? PL::T : 1];      // the peer's half of L(1) (its local L(0)), pass-0 thread positions
+    uint32_t ptu[SP ? PL::NW : 1];                 // the peer's transformed pinned hard output (G-check)
+    uint32_t pxh[SP ? PL::NW : 1];                 // the peer's x_hat words
+    int pst[4];                                    // the peer's frontier (global), completion stage, frame-end sums
+    long long pfin[3];                             // frame end (from the second CTA): bit errors, PEs, events
+    uint32_t tu[SP ? PL::NW : 1];                  // own transformed pinned hard output
+    unsigned long long post;                       // second CTA: the first CTA's post (seq << 32 | frontier << 16 | code)
+    unsigned long long postv;                      // its broadcast copy
 };
 
 // XH: also record each freeze event's x_hat (trace calls; a separate
 // instantiation keeps the decode kernel's code unchanged)
-template <int M, int KIND, bool XH = false>
+template <int M, int KIND, bool XH = false, bool SP = false>
 struct Dec {
-    using PL = Plan<M>;
-    using C = Cfg<M>;
+    using PL = Plan<M, SP>;
+    using C = Cfg<M, SP>;
     static constexpr int N = PL::N, P = PL::P, K = PL::K, Q = PL::Q, NW = PL::NW, kT = PL::T;
     static constexpr bool csfg = KIND == 2;
 
-    Smem<M>* sm;
+    Smem<M, SP>* sm;
     const DecodeArgs* a;
     float* Lg;  // L2 levels, N floats each
     uint32_t tb;  // this warp's TMEM columns (TMEM levels at tb + P * slot)
-    static constexpr bool kTpReg = TprotReg<M>::value;
+    static constexpr bool kTpReg = TprotReg<C>::value;
     uint32_t tpr[kTpReg && PL::NTM > 0 ? PL::NTM : 1];  // boundary masks of the TMEM levels (kTpReg)
     __device__ __forceinline__ uint32_t& tprot(int k) { return kTpReg ? tpr[k] : sm->tprot[k][tid]; }
     const float* llr;
@@ -205,6 +270,23 @@ struct Dec {
     FzT snap;      // sign bits of R(S+1) after each stage of the current pass
     uint32_t onm;  // PE activations of the current pass, bit i * P/2 + k
     unsigned act;  // this thread's PE activations (< 2^32 per frame)
+    // SP (one half of a frame on a 2-CTA cluster)
+    int rank;       // 0: the frame's rows [0, N), 1: rows [N, 2N)
+    int gfr;        // the frame's frontier, 0 .. 2N (frontier = this half's part of it)
+    int cut;        // second CTA: first local stage the reference did not run in the final sweep (frame complete)
+    int xcode;      // first CTA: 1 + stage index of the pass at which its frontier reached N, else 0
+    bool hfz;       // this half frozen whole by a commit of the frame's stage 0
+    bool nowait;    // second CTA: the frontier cannot reach N in the rest of this sweep
+    uint32_t rsm;   // the peer's shared memory (cluster window address of its Smem)
+
+    // the frame's frontier lies in this half: its candidate blocks are checked here
+    __device__ __forceinline__ bool owner() const { return !SP || (gfr >> PL::M) == rank; }
+    // the reference left the stage loop (csfg_freeze.cpp:109): the frame's frontier reached its end
+    __device__ __forceinline__ bool ended() const { return SP ? (rank == 1 && frontier >= N) : frontier >= N; }
+    template <typename F>
+    __device__ __forceinline__ uint32_t peer_addr(const F* field) const {
+        return rsm + (uint32_t)((const char*)field - (const char*)sm);
+    }
 
     template <int q>
     __device__ __forceinline__ int row(int j) const {
@@ -284,7 +366,7 @@ struct Dec {
         constexpr int dj = 1 << (g - b);
         constexpr int i = S - q * K;  // stage index inside the pass
         if constexpr (csfg) {
-            if (frontier >= N) return false;
+            if (ended()) return false;
             if constexpr (i == 0) {
                 snap = 0;
                 onm = 0u;
@@ -304,7 +386,9 @@ struct Dec {
                 ++k;
             }
         }
-        constexpr bool tin = C::where(S + 1) == kTmem, tout = S > 0 && C::where(S) == kTmem;
+        // SP: local L(0) is the frame's L(1): stored (TMEM) for the next cross stage and pushed to the peer
+        constexpr bool l0out = SP && S == 0;
+        constexpr bool tin = C::where(S + 1) == kTmem, tout = (S > 0 && C::where(S) == kTmem) || l0out;
         float tl[tin ? P : 1], to[tout ? P : 1];
         if constexpr (tin) {
             tm::wait_st();  // this level's store of the previous sweep / its boundary fix-up
@@ -354,7 +438,7 @@ struct Dec {
             const float n_b = __fadd_rn(r_b, cross);
             R[j] = on ? n_t : r_t;
             R[j + dj] = on ? n_b : r_b;
-            if constexpr (S == 0 && KIND != 0) {
+            if constexpr (S == 0 && KIND != 0 && !SP) {
                 // pass 0: a warp's lanes hold 32 consecutive rows of every register
                 const uint32_t wt = __ballot_sync(kFull, xt), wb = __ballot_sync(kFull, xb);
                 if (lane == 0) {
@@ -364,7 +448,12 @@ struct Dec {
             }
             ++k;
         }
-        if constexpr (tout) tm::st16(tb + P * PL::slot(S), to);
+        if constexpr (l0out) {
+            tm::st16(tb + P * PL::L0S, to);
+            push_l0(to);
+        } else if constexpr (tout) {
+            tm::st16(tb + P * PL::slot(S), to);
+        }
         act += __popc(onb);
         if constexpr (csfg) {
             onm |= onb << (i * (P / 2));
@@ -482,6 +571,22 @@ struct Dec {
     __device__ __forceinline__ void pass_check() {
         constexpr int b = PL::base(q);
         constexpr int nst = PL::last(q) - q * K + 1;
+        int first = 0;  // first stage index of the pass whose candidate this CTA checks
+        if constexpr (SP) {
+            if (!owner()) {
+                if (rank == 0) {  // the frontier moved to the second half
+                    __syncthreads();  // (orders the pass-boundary R exchange, as the check's barriers do)
+                    return;
+                }
+                if (nowait) {
+                    __syncthreads();
+                    return;
+                }
+                first = take_over<q>();
+                if (first > nst) return;  // the first CTA still holds the frontier after this pass
+            }
+            xcode = 0;
+        }
         FzT W = pass_bits<q, 0>();
         W = lane_transform<(b < 5 ? b : 5)>(W);
         if constexpr (b > 5) W = warp_transform<b - 5>(W);
@@ -494,24 +599,28 @@ struct Dec {
         bad = sm->vw[ph];
         if (tid == 0) sm->vw[ph == 0 ? 2 : ph - 1] = 0u;  // used two checks from now
         ph = ph == 2 ? 0 : ph + 1;
-        if (bad == (1u << ((1 << nst) - 1)) - 1u) return;  // every candidate rejected
+        if (bad == (1u << ((1 << nst) - 1)) - 1u) {  // every candidate rejected
+            if constexpr (SP) post<q + 1>();
+            return;
+        }
         bool any = false;
-        commit_walk<q, 0>(W, bad, 0, any);
+        commit_walk<q, 0>(W, bad, 0, any, first);
+        if constexpr (SP) post<q + 1>();
         // freeze stages are read in another layout by the next pass
         if (any) __syncthreads();
     }
 
     template <int q, int i>
-    __device__ __forceinline__ void commit_walk(FzT W, uint32_t bad, int v, bool& any) {
+    __device__ __forceinline__ void commit_walk(FzT W, uint32_t bad, int v, bool& any, int first) {
         constexpr int S = q * K + i;
         if constexpr (S <= PL::last(q)) {
             if (frontier >= N) return;
-            if (!((bad >> ((1 << i) - 1 + v)) & 1u)) {
+            if (i >= first && !((bad >> ((1 << i) - 1 + v)) & 1u)) {
                 commit<q, i>(W);
                 v |= 1 << i;
                 any = true;
             }
-            commit_walk<q, i + 1>(W, bad, v, any);
+            commit_walk<q, i + 1>(W, bad, v, any, first);
         }
     }
 
@@ -559,7 +668,7 @@ struct Dec {
                     atomicOr(&a->ev_xhat[((long long)sm->frame * a->ev_cap + nev) * NW + (r >> 5)], bit);
             }
         }
-        if (tid == 0 && a->events && nev < a->ev_cap) {
+        if (!SP && tid == 0 && a->events && nev < a->ev_cap) {
             int* e = a->events + ((long long)sm->frame * a->ev_cap + nev) * 5;
             e[0] = it;
             e[1] = S;
@@ -569,7 +678,14 @@ struct Dec {
         }
         nev += 1;
         frontier = start + sz;
-        uncount<q, i + 1>(bm, frontier >= N);
+        if constexpr (SP) {
+            gfr = rank * N + frontier;
+            if (frontier >= N) {
+                if (rank == 0) xcode = i + 1;  // the second CTA checks from stage index i + 1 on
+                else cut = S + 1;              // the frame is complete: its stage S + 2 (local S + 1) never ran
+            }
+        }
+        uncount<q, i + 1>(bm, ended());
     }
 
     template <int q, int i>
@@ -608,6 +724,142 @@ struct Dec {
         }
     }
 
+    // ---- SP: the pair protocol -------------------------------------------
+    // The first CTA owns the frontier until it reaches N. It posts its
+    // frontier after the check of the frame's stage 0 and after each pass
+    // (seq = it * (Q + 1) + phase, phase 0 = the cross stage's check, q + 1 =
+    // pass q; code = 1 + the stage index at which the frontier left the first
+    // half). The second CTA's checks of pass q wait for that pass's post only
+    // while a crossing in pass q is possible: candidate blocks are aligned, so
+    // a frontier below N - (block size of the pass's first stage) at the
+    // pass's start stays below it for the rest of the sweep (every later
+    // block is smaller) -- then it stops waiting until the next sweep.
+    // After the frontier crossed, neither waits.
+
+    // local L(0) of this sweep (the frame's L(1)) into the peer's mailbox
+    __device__ __forceinline__ void push_l0(const float* v) const {
+#pragma unroll
+        for (int j = 0; j < P; ++j) st_peer(peer_addr(&sm->mb[j][tid]), v[j]);
+    }
+
+    template <int PH>
+    __device__ __forceinline__ void post() const {
+        if (rank == 0 && tid == 0)
+            st_peer(peer_addr(&sm->post), ((unsigned long long)(it * (Q + 1) + PH) << 32) |
+                                              ((unsigned long long)frontier << 16) | (unsigned long long)xcode);
+    }
+
+    // second CTA before owning the frontier: the first stage index of pass q
+    // it checks (> the pass's stage count: none, the first half still holds it)
+    template <int q>
+    __device__ __forceinline__ int take_over() {
+        const uint32_t s0 = (uint32_t)it * (Q + 1), sq0 = s0 + q, sq1 = sq0 + 1;
+        constexpr int bound = N - (N >> (q * K + 1));  // a frontier below it cannot cross in pass q or later
+        if (tid == 0) {
+            unsigned long long w;
+            do {  // the frontier at the start of pass q (or a crossing of this sweep)
+                w = ld_volatile(&sm->post);
+            } while ((uint32_t)(w >> 32) < sq0 && !((w & 0xffffu) && (uint32_t)(w >> 32) >= s0));
+            if ((uint32_t)(w >> 32) == sq0 && !(w & 0xffffu) && (int)((w >> 16) & 0xffffu) >= bound) {
+                do {  // a crossing in pass q is possible: its verdict
+                    w = ld_volatile(&sm->post);
+                } while ((uint32_t)(w >> 32) < sq1);
+            }
+            sm->postv = w;
+        }
+        __syncthreads();
+        const unsigned long long w = sm->postv;
+        const uint32_t seq = (uint32_t)(w >> 32);
+        const int code = (int)(w & 0xffffu);
+        if (code && (seq == sq1 || (q == 0 && seq == s0))) {
+            gfr = N;  // the frame's frontier is this half's row 0
+            return seq == s0 ? 0 : code;
+        }
+        if (seq == sq0 && !code) nowait = true;  // (the bound held: no crossing in this sweep)
+        return 1 << 30;
+    }
+
+    // The frame's stage 0 (distance N, bp_core.cpp:18-32, always active): row r
+    // of both halves meets at the same thread position of both CTAs. R(1) of
+    // this half goes to R (pass 0's layout), x_hat = (R(0) + L(0) < 0) of this
+    // half to sm->xh (bp_core.cpp:99); its PEs are counted by the first CTA.
+    __device__ __forceinline__ void cross_stage() {
+        float lo[P];
+        tm::wait_st();
+        tm::ld16(tb + P * PL::L0S, lo);
+        tm::wait_ld();
+        const float* own = llr + (long long)rank * N;
+        const float* oth = llr + (long long)(rank ^ 1) * N;
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            const int r = row<0>(j);
+            const float mine = __fadd_rn(own[r], 0.0f), peer = __fadd_rn(oth[r], 0.0f);
+            const float lp = sm->mb[j][tid];
+            const float lt = rank == 0 ? lo[j] : lp, lb = rank == 0 ? lp : lo[j];
+            const float r_t = rank == 0 ? mine : peer, r_b = rank == 0 ? peer : mine;
+            const float cross = __fmul_rn(alpha, xsmin(lt, r_t));
+            const float sum_bot = __fadd_rn(lb, r_b);
+            float rn, x;
+            if (rank == 0) {
+                const float l_top = __fmul_rn(alpha, xsmin(lt, sum_bot));
+                rn = __fmaf_rn(alpha, xsmin(r_t, sum_bot), 0.0f);
+                x = __fadd_rn(r_t, l_top);
+            } else {
+                const float l_bot = __fadd_rn(lb, cross);
+                rn = __fadd_rn(r_b, cross);
+                x = __fadd_rn(r_b, l_bot);
+            }
+            R[j] = rn;
+            const uint32_t w = __ballot_sync(kFull, x < 0.f);
+            if (lane == 0) sm->xh[r >> 5] = w;
+        }
+        if (rank == 0) act += P;
+    }
+
+    // candidate_block of the frame's stage 0 (this half, size N) and its
+    // check/commit (csfg_freeze.cpp:18-39, 82-93) on R(1): the transform over
+    // every row bit of the half (register, lane and warp bits of pass 0)
+    __device__ __forceinline__ void cross_check() {
+        const uint32_t x = sign_bits();
+        uint32_t u = bits_transform<K>(x);
+        u = lane_transform<5>(u);
+        u = warp_transform<PL::LOGT - 5>(u);
+        if (__syncthreads_or((u & fz<0>()) != 0u)) return;
+        // apply_freeze: L(1) = +-CAP over the half, freeze stage 0 (every later
+        // stage of the half inactive: its local sweeps stop), decided_u = u
+        hfz = true;
+        float v[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            v[j] = ((x >> j) & 1u) ? -kCap : kCap;
+            const uint32_t w = __ballot_sync(kFull, (u >> j) & 1u);
+            if (lane == 0) sm->dec[row<0>(j) >> 5] = w;
+        }
+        tm::st16(tb + P * PL::L0S, v);
+        nev += 1;
+        frontier = N;
+        gfr = rank * N + N;
+        if (rank == 1) {
+            cut = 0;  // the frame is complete: no stage after its stage 0 ran
+        } else {
+            xcode = 1;
+        }
+    }
+
+    // PE activations of local stages >= l0 under the final freeze stages
+    // (first CTA, when the second half completed the frame mid-sweep)
+    __device__ __forceinline__ unsigned recount_from(int l0) const {
+        unsigned c = 0;
+        for (int l = l0; l < M; ++l) {
+            const int g = M - 1 - l;
+            for (int p = tid; p < N / 2; p += kT) {
+                const int r = ((p >> g) << (g + 1)) | (p & ((1 << g) - 1));
+                c += (int)sm->fst[r] >= l ? 1u : 0u;
+            }
+        }
+        return c;
+    }
+
     template <int S>
     __device__ __forceinline__ bool sweep_from() {
         if (!stage<S>()) return false;
@@ -640,7 +892,7 @@ struct Dec {
         return !__syncthreads_or(u != x);
     }
 
-    __device__ void run(const DecodeArgs& args, Smem<M>* s) {
+    __device__ void run(const DecodeArgs& args, Smem<M, SP>* s) {
         a = &args;
         sm = s;
         tid = threadIdx.x;
@@ -788,7 +1040,235 @@ struct Dec {
             }
         }
     }
+
+    // SP: one half of each frame of length 2N on a 2-CTA cluster (csfg).
+    // Per iteration: the cross stage (the frame's stage 0) from the peer's
+    // L(1) in the mailbox, the check of the frame's stage-0 candidate by the
+    // half holding the frontier, the local sweep (the frame's stages 1..m-1,
+    // whose local stage 0 pushes the new L(1) into the peer's mailbox), the
+    // pinned G-check over both halves (csfg_freeze.cpp:120-135: the frame's
+    // transform is the halves' local transforms plus one XOR level across
+    // the pair). Two cluster barriers per iteration: after the cross stage
+    // (the mailbox is consumed before the peer refills it) and at the end
+    // (mailbox, G-check words and frontier exchanged).
+    __device__ void run_pair(const DecodeArgs& args, Smem<M, SP>* s) {
+        a = &args;
+        sm = s;
+        tid = threadIdx.x;
+        lane = tid & 31;
+        warp = tid >> 5;
+        alpha = args.alpha;
+        rank = cluster_rank();
+        rsm = cluster_map(sm, rank ^ 1);
+        constexpr int N2 = 2 * N;
+        init_fz<0>(args.frozen_rows + (long long)rank * N);
+        for (;;) {
+            // the previous frame is done in both CTAs: reset what the peer writes
+            if (rank == 1 && tid == 0) sm->post = 0u;
+#pragma unroll
+            for (int j = 0; j < P; ++j) sm->mb[j][tid] = 0.f;  // the peer's L(1) (init_state: 0)
+            cluster_sync();
+            if (rank == 0 && tid == 0) {
+                const unsigned long long idx = atomicAdd(args.queue, 1ull);
+                const long long v = (long long)idx < args.frames ? (long long)idx : -1;
+                sm->frame = v;
+                st_peer(peer_addr(&sm->frame), v);
+            }
+            cluster_sync();
+            const long long f = sm->frame;
+            if (f < 0) break;
+            // both CTAs test the whole frame (their own rows and the peer's at
+            // the same positions), so they agree without an exchange
+            llr = args.llr + f * (long long)N2;
+            bool bad = false;
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                bad |= !(fabsf(llr[row<0>(j)]) <= kClampFreeBound);
+                bad |= !(fabsf(llr[N + row<0>(j)]) <= kClampFreeBound);
+            }
+            if (__syncthreads_or(bad)) {
+                if (rank == 0 && tid == 0) {
+                    const unsigned long long slot = atomicAdd(args.list_len, 1ull);
+                    args.list[slot] = f + args.frame_base;
+                }
+                continue;
+            }
+            // init_state (bp_core.cpp:43-56)
+#pragma unroll
+            for (int l = 0; l < PL::NREG; ++l)
+#pragma unroll
+                for (int j = 0; j < P; ++j) Lr[l][j] = 0.f;
+            lm_nz = fz<Q - 1>();
+            lm_neg = 0u;
+#pragma unroll
+            for (int j = 0; j < P; ++j) R[j] = 0.f;
+            for (int i = tid; i < PL::NSM * PL::NX; i += kT) (&sm->Ls[0][0])[i] = 0.f;
+            {
+                float z[P];
+#pragma unroll
+                for (int j = 0; j < P; ++j) z[j] = 0.f;
+#pragma unroll
+                for (int k = 0; k < PL::NTM; ++k) {
+                    tm::st16(tb + P * k, z);
+                    tprot(k) = 0u;
+                }
+                tm::st16(tb + P * PL::L0S, z);
+            }
+            for (int r = tid; r < N; r += kT) sm->fst[r] = kNotFrozen;
+            for (int w = tid; w < NW; w += kT) sm->dec[w] = 0u;
+            frontier = 0;
+            gfr = 0;
+            cut = M;
+            xcode = 0;
+            hfz = false;
+            nev = 0;
+            ph = 0;
+            if (tid < 3) sm->vw[tid] = 0u;
+            act = 0;
+            __syncthreads();
+            int iters = 0;
+            bool converged = false;
+            for (int t = 1; t <= args.max_iter; ++t) {
+                if (gfr >= N2 || converged) break;
+                iters = t;
+                it = t;
+                asm volatile("" : "+r"(tid));
+                cross_stage();
+                cluster_arrive();  // this CTA consumed its mailbox
+                nowait = false;
+                if (owner()) {
+                    xcode = 0;
+                    cross_check();
+                    post<0>();  // (first CTA) its frontier after the frame's stage-0 check
+                }
+                cluster_wait();  // so did the peer: L(1) of this sweep may go to it
+                if (hfz) {
+                    float v[P];
+                    tm::ld16(tb + P * PL::L0S, v);
+                    tm::wait_ld();
+                    push_l0(v);
+                } else {
+                    sweep_from<0>();
+                    if constexpr (PL::NTM > 0) fixup_tmem();
+                }
+                // pinned G-check inputs: this half's hard output (rows < frontier
+                // from decided_u), transformed over the half's row bits
+                uint32_t g = bits_transform<K>(u_group(frontier));
+                g = lane_transform<5>(g);
+                g = warp_transform<PL::LOGT - 5>(g);
+                const int r0 = P * tid;
+                uint32_t word = g << (r0 & 31);
+#pragma unroll
+                for (int o = 1; o < 32 / P; o <<= 1) word |= __shfl_xor_sync(kFull, word, o);
+                if ((r0 & 31) == 0) {
+                    sm->tu[r0 >> 5] = word;
+                    st_peer(peer_addr(&sm->ptu[r0 >> 5]), word);
+                }
+                if (tid < NW) st_peer(peer_addr(&sm->pxh[tid]), sm->xh[tid]);
+                if (tid == 0) {
+                    st_peer(peer_addr(&sm->pst[0]), gfr);
+                    st_peer(peer_addr(&sm->pst[1]), cut);
+                }
+                cluster_sync();
+                const int pg = sm->pst[0];
+                if (rank == 0) cut = sm->pst[1];
+                gfr = max(gfr, pg);
+                if (gfr < N2) {
+                    // x = the frame's transform: first half t0 ^ t1, second half t1
+                    bool mm = false;
+                    if (tid < NW) {
+                        const uint32_t t0 = rank == 0 ? sm->tu[tid] : sm->ptu[tid];
+                        const uint32_t t1 = rank == 0 ? sm->ptu[tid] : sm->tu[tid];
+                        const uint32_t h0 = rank == 0 ? sm->xh[tid] : sm->pxh[tid];
+                        const uint32_t h1 = rank == 0 ? sm->pxh[tid] : sm->xh[tid];
+                        mm = ((t0 ^ t1) != h0) || (t1 != h1);
+                    }
+                    converged = !__syncthreads_or(mm);
+                }
+            }
+            const int stop = (gfr >= N2) ? 2 : (converged ? 1 : 0);
+            // the second half completed the frame mid-sweep: the first half's
+            // stages after that point are not the reference's
+            if (rank == 0 && gfr >= N2 && !hfz && cut < M) act -= recount_from(cut);
+            __syncthreads();  // decided_u of the last commits
+            uint32_t u;
+            const int r0 = P * tid;
+            if (gfr >= N2) u = (sm->dec[r0 >> 5] >> (r0 & 31)) & low_mask(P);
+            else u = u_group(frontier);
+            uint32_t word = u << (r0 & 31);
+#pragma unroll
+            for (int o = 1; o < 32 / P; o <<= 1) word |= __shfl_xor_sync(kFull, word, o);
+            int berr = 0;
+            if ((r0 & 31) == 0) {
+                const int wi = rank * NW + (r0 >> 5);
+                if (args.u_bits) args.u_bits[f * 2 * NW + wi] = word;
+                if (args.truth_u) berr = __popc((word ^ args.truth_u[f * 2 * NW + wi]) & ~args.frozen_bits[wi]);
+            }
+            berr = __reduce_add_sync(kFull, berr);
+            const unsigned wact = __reduce_add_sync(kFull, act);
+            if (lane == 0) {
+                sm->buf[2 * warp] = (uint32_t)berr;
+                sm->buf[2 * warp + 1] = wact;
+            }
+            __syncthreads();
+            long long pe = 0;
+            int be = 0;
+            if (tid == 0) {
+                for (int w = 0; w < PL::NWARP; ++w) {
+                    be += (int)sm->buf[2 * w];
+                    pe += sm->buf[2 * w + 1];
+                }
+                if (rank == 1) {
+                    st_peer(peer_addr(&sm->pfin[0]), (long long)be);
+                    st_peer(peer_addr(&sm->pfin[1]), pe);
+                    st_peer(peer_addr(&sm->pfin[2]), (long long)nev);
+                }
+            }
+            cluster_sync();
+            if (rank == 0 && tid == 0) {
+                be += (int)sm->pfin[0];
+                pe += sm->pfin[1];
+                const int ne = nev + (int)sm->pfin[2];
+                if (args.iters) args.iters[f] = iters;
+                if (args.pe) args.pe[f] = pe;
+                if (args.stop) args.stop[f] = (uint8_t)stop;
+                if (args.nev) args.nev[f] = ne;
+                if (args.counters) {
+                    unsigned long long* cs = counter_set(args, f);
+                    atomicAdd(&cs[kCntFrames], 1ull);
+                    atomicAdd(&cs[kCntBitErr], (unsigned long long)be);
+                    atomicAdd(&cs[kCntFrameErr], be > 0 ? 1ull : 0ull);
+                    atomicAdd(&cs[kCntIters], (unsigned long long)iters);
+                    atomicAdd(&cs[kCntItersSq], (unsigned long long)iters * iters);
+                    atomicAdd(&cs[kCntPe], (unsigned long long)pe);
+                    atomicAdd(&cs[kCntEvents], (unsigned long long)ne);
+                    atomicAdd(&cs[kCntStop0 + stop], 1ull);
+                }
+            }
+        }
+    }
 };
+
+// SP kernel: a 2-CTA cluster per frame of length 2^(M+1), each CTA one half
+template <int M, int KIND>
+__global__ void __launch_bounds__(Plan<M, true>::T, 1) bp_pair_kernel(const __grid_constant__ DecodeArgs a) {
+    extern __shared__ __align__(16) unsigned char csm[];
+    using PL = Plan<M, true>;
+    Dec<M, KIND, false, true> dec;
+    Smem<M, true>* sm = reinterpret_cast<Smem<M, true>*>(csm);
+    constexpr int COLS = Cfg<M, true>::TMEM_COLS;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) tm::alloc<COLS>(&sm->tbase);
+    tm::fence_before();
+    __syncthreads();
+    tm::fence_after();
+    dec.tb = sm->tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(PL::TM_WCOLS * (warp >> 2));
+    dec.run_pair(a, sm);
+    tm::fence_before();
+    __syncthreads();
+    tm::fence_after();
+    if (warp == 0) tm::dealloc<COLS>(sm->tbase);
+}
 
 template <int M, int KIND, bool XH = false>
 __global__ void __launch_bounds__(Plan<M>::T, Cfg<M>::MINB) bp_cta_kernel(const __grid_constant__ DecodeArgs a) {
@@ -840,6 +1320,43 @@ static cudaError_t launch_m(const DecodeArgs& a, int grid, cudaStream_t st) {
     }
 }
 
+// SP launch: clusters of two CTAs, as many as can be resident (one per SM
+// pair), each taking frames from the queue
+template <int M, int KIND>
+static cudaError_t launch_pair(const DecodeArgs& a, cudaStream_t st) {
+    auto k = bp_pair_kernel<M, KIND>;
+    const size_t smem = sizeof(Smem<M, true>);
+    static_assert(sizeof(Smem<M, true>) <= 227 * 1024, "one half-frame CTA per SM");
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(Plan<M, true>::T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static int max_clusters = 0;  // per process (one device model)
+    if (!max_clusters) {
+        cfg.gridDim = dim3(2 * 74);
+        int nc = 0;
+        e = cudaOccupancyMaxActiveClusters(&nc, k, &cfg);
+        if (e != cudaSuccess) return e;
+        if (nc < 1) return cudaErrorInvalidConfiguration;
+        max_clusters = nc;
+    }
+    long long ncl = std::min<long long>(max_clusters, a.frames);
+    if (const char* gc = getenv("PBP_GRID_CAP")) ncl = std::max(1ll, std::min(ncl, atoll(gc) / 2));  // experiments
+    cfg.gridDim = dim3((unsigned)(2 * ncl));
+    e = cudaLaunchKernelEx(&cfg, k, a);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 template <int M, int KIND>
 static int occ_t() {
     int nb = 0;
@@ -870,7 +1387,17 @@ long long cta_scratch_floats(int m) {
     return 0;
 }
 
+// n = 16384 csfg decodes (no event trace) on 2-CTA clusters, one half of the
+// frame per SM: every message level on chip (PBP_PAIR=0: one CTA per frame)
+bool cta_pair_on(int m, int kind) {
+    const char* e = getenv("PBP_PAIR");  // read per launch: tests compare both layouts in one process
+    return (e ? atoi(e) : 1) && m == 14 && kind == 2;
+}
+static bool cta_pair(const DecodeArgs& a) { return cta_pair_on(a.m, a.kind) && !a.events && !a.ev_xhat; }
+size_t cta_pair_smem_bytes() { return sizeof(cta::Smem<13, true>); }
+
 cudaError_t launch_cta(const DecodeArgs& a, int grid, cudaStream_t st) {
+    if (cta_pair(a)) return cta::launch_pair<13, 2>(a, st);
     switch (a.m) {
         case 11: return cta::launch_m<11>(a, grid, st);
         case 12: return cta::launch_m<12>(a, grid, st);

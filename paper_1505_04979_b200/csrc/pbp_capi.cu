@@ -32,6 +32,8 @@ cudaError_t launch_cta(const DecodeArgs& a, int grid, cudaStream_t st);
 int cta_blocks_per_sm(int m, int kind);
 size_t cta_smem_bytes(int m);
 int cta_warps(int m);
+bool cta_pair_on(int m, int kind);
+size_t cta_pair_smem_bytes();
 cudaError_t launch_channel(const GenArgs& g, int grid, cudaStream_t stream);
 long long channel_seed_words(long long count);
 }  // namespace pbp
@@ -560,6 +562,9 @@ int pbp_kernel_info(int32_t n, int decoder, int32_t* smem_bytes, int32_t* warps_
     if (pbp::warp_kernel_supported(m)) {
         if (smem_bytes) *smem_bytes = (int32_t)pbp::warp_smem_bytes(m, decoder);
         if (warps_per_sm) *warps_per_sm = pbp::warp_blocks_per_sm(m, decoder) * pbp::warp_kernel_warps(m);
+    } else if (pbp::cta_pair_on(m, decoder)) {  // half a frame per CTA (2-CTA clusters), one CTA per SM
+        if (smem_bytes) *smem_bytes = (int32_t)pbp::cta_pair_smem_bytes();
+        if (warps_per_sm) *warps_per_sm = pbp_device_count() > 0 ? 16 : 0;
     } else if (pbp::cta_kernel_supported(m)) {  // CTA per frame: shared bytes per CTA, resident warps
         if (smem_bytes) *smem_bytes = (int32_t)pbp::cta_smem_bytes(m);
         if (warps_per_sm) *warps_per_sm = pbp::cta_blocks_per_sm(m, decoder) * pbp::cta_warps(m);
@@ -577,6 +582,11 @@ int pbp_ctx_force_generic(pbp_ctx* ctx, int on) {
 }
 
 int pbp_kernel_path(int32_t n) { return is_pow2(n) ? fast_kernel(log2i(n)) : 0; }
+
+int pbp_kernel_cluster(int32_t n, int decoder) {
+    if (!is_pow2(n) || !fast_kernel(log2i(n))) return 0;
+    return pbp::cta_pair_on(log2i(n), decoder) ? 2 : 1;
+}
 
 int pbp_last_launch_info(pbp_ctx* ctx, int32_t* launches, int64_t* rerouted) {
     if (!ctx) return fail(PBP_EINVAL, "null context");
