@@ -35,6 +35,7 @@
 // clamp-free bound or non-finite are re-routed to the generic kernel, which
 // keeps every clamp.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -72,14 +73,13 @@ struct Cfg<12> {  // 256 x 16, two frames per SM: four levels in registers, five
     }
 };
 template <>
-struct Cfg<13> {  // 512 x 16: three levels in registers, five in shared memory, four in TMEM (all on chip)
+struct Cfg<13> {  // 512 x 16: three levels in registers, three in shared memory, six in TMEM (all on chip)
     static constexpr int LOGT = 9, K = 4, MINB = 1;
     static constexpr bool r0reg = false, rx2 = false;
     static constexpr int TMEM_COLS = 512;  // 16 warps: 128 columns of its lane quarter per warp
     static constexpr bool TPROT_REG = false;
-    static constexpr int where(int s) {
-        return s == 13 ? kBits : (s <= 3) ? kReg : (s % 4 == 0 || s == 5 || s == 6) ? kSmem : kTmem;
-    }
+    // the inner levels of passes 1 and 2 in TMEM (5 and 6 in shared memory measured 1.8 % slower)
+    static constexpr int where(int s) { return s == 13 ? kBits : (s <= 3) ? kReg : (s % 4 == 0) ? kSmem : kTmem; }
 };
 template <>
 struct Cfg<14> {  // 1024 x 16: one level in shared memory, four in TMEM, the rest in L2
@@ -230,10 +230,10 @@ struct Smem {
     uint32_t tprot[(PL::NTM > 0 && !TprotReg<C>::value) ? PL::NTM : 1][(PL::NTM > 0 && !TprotReg<C>::value) ? PL::T : 1];
     uint32_t tbase;                                // TMEM allocation
     // SP: what the peer CTA of the pair writes here (st.shared::cluster)
-    float mb[SP ? PL::P : 1][SP ? PL::T : 1];      // the peer's half of L(1) (its local L(0)), pass-0 thread positions
-    uint32_t ptu[SP ? PL::NW : 1];                 // the peer's transformed pinned hard output (G-check)
-    uint32_t pxh[SP ? PL::NW : 1];                 // the peer's x_hat words
-    int pst[4];                                    // the peer's frontier (global), completion stage, frame-end sums
+    // double-buffered by iteration parity: the peer writes sweep t's while this CTA may still read t-1's
+    float mb[SP ? 2 : 1][SP ? PL::P : 1][SP ? PL::T : 1];  // the peer's half of L(1) (its local L(0)), pass-0 thread positions
+    uint32_t gx[SP ? 2 : 1][SP ? PL::NW : 1];     // G-check words from the peer (first CTA: t1; second: t0 ^ x_hat0)
+    int pst[2][4];                                 // the peer's frontier (global), completion stage, mismatch of its half
     long long pfin[3];                             // frame end (from the second CTA): bit errors, PEs, events
     uint32_t tu[SP ? PL::NW : 1];                  // own transformed pinned hard output
     unsigned long long post;                       // second CTA: the first CTA's post (seq << 32 | frontier << 16 | code)
@@ -277,12 +277,16 @@ struct Dec {
     int xcode;      // first CTA: 1 + stage index of the pass at which its frontier reached N, else 0
     bool hfz;       // this half frozen whole by a commit of the frame's stage 0
     bool nowait;    // second CTA: the frontier cannot reach N in the rest of this sweep
+    bool xpend;     // the frame's stage-0 check of this sweep is pending (decided with pass 0's checks)
+    uint32_t x0;    // its hard decisions: sign bits of R(1) of this half (pass 0's layout)
+    unsigned act0;  // PE activations before this sweep's local stages
     uint32_t rsm;   // the peer's shared memory (cluster window address of its Smem)
 
     // the frame's frontier lies in this half: its candidate blocks are checked here
     __device__ __forceinline__ bool owner() const { return !SP || (gfr >> PL::M) == rank; }
     // the reference left the stage loop (csfg_freeze.cpp:109): the frame's frontier reached its end
-    __device__ __forceinline__ bool ended() const { return SP ? (rank == 1 && frontier >= N) : frontier >= N; }
+    // (SP: or this half was frozen whole at the frame's stage 0 in this sweep)
+    __device__ __forceinline__ bool ended() const { return SP ? (hfz || (rank == 1 && frontier >= N)) : frontier >= N; }
     template <typename F>
     __device__ __forceinline__ uint32_t peer_addr(const F* field) const {
         return rsm + (uint32_t)((const char*)field - (const char*)sm);
@@ -573,6 +577,16 @@ struct Dec {
         constexpr int nst = PL::last(q) - q * K + 1;
         int first = 0;  // first stage index of the pass whose candidate this CTA checks
         if constexpr (SP) {
+            if (q == 0 && xpend) {
+                // the frame's stage-0 candidate (csfg_freeze.cpp:111-118 at stage 0), decided
+                // before pass 0's candidates: an accept makes this sweep's local stages
+                // void (every PE of the half inactive), so they are uncounted
+                xpend = false;
+                xcode = 0;
+                const bool acc = cross_check();
+                post<0>();  // (first CTA) its frontier after the frame's stage-0 check
+                if (acc) return;
+            }
             if (!owner()) {
                 if (rank == 0) {  // the frontier moved to the second half
                     __syncthreads();  // (orders the pass-boundary R exchange, as the check's barriers do)
@@ -739,7 +753,7 @@ struct Dec {
     // local L(0) of this sweep (the frame's L(1)) into the peer's mailbox
     __device__ __forceinline__ void push_l0(const float* v) const {
 #pragma unroll
-        for (int j = 0; j < P; ++j) st_peer(peer_addr(&sm->mb[j][tid]), v[j]);
+        for (int j = 0; j < P; ++j) st_peer(peer_addr(&sm->mb[it & 1][j][tid]), v[j]);
     }
 
     template <int PH>
@@ -794,7 +808,7 @@ struct Dec {
         for (int j = 0; j < P; ++j) {
             const int r = row<0>(j);
             const float mine = __fadd_rn(own[r], 0.0f), peer = __fadd_rn(oth[r], 0.0f);
-            const float lp = sm->mb[j][tid];
+            const float lp = sm->mb[(it - 1) & 1][j][tid];
             const float lt = rank == 0 ? lo[j] : lp, lb = rank == 0 ? lp : lo[j];
             const float r_t = rank == 0 ? mine : peer, r_b = rank == 0 ? peer : mine;
             const float cross = __fmul_rn(alpha, xsmin(lt, r_t));
@@ -819,15 +833,17 @@ struct Dec {
     // candidate_block of the frame's stage 0 (this half, size N) and its
     // check/commit (csfg_freeze.cpp:18-39, 82-93) on R(1): the transform over
     // every row bit of the half (register, lane and warp bits of pass 0)
-    __device__ __forceinline__ void cross_check() {
-        const uint32_t x = sign_bits();
+    __device__ __forceinline__ bool cross_check() {
+        const uint32_t x = x0;
         uint32_t u = bits_transform<K>(x);
         u = lane_transform<5>(u);
         u = warp_transform<PL::LOGT - 5>(u);
-        if (__syncthreads_or((u & fz<0>()) != 0u)) return;
-        // apply_freeze: L(1) = +-CAP over the half, freeze stage 0 (every later
-        // stage of the half inactive: its local sweeps stop), decided_u = u
+        if (__syncthreads_or((u & fz<0>()) != 0u)) return false;
+        // apply_freeze: L(1) = +-CAP over the half (over the speculative values
+        // local stage 0 stored and pushed), freeze stage 0 (every later stage of
+        // the half inactive: its local sweeps stop), decided_u = u
         hfz = true;
+        act = act0;
         float v[P];
 #pragma unroll
         for (int j = 0; j < P; ++j) {
@@ -835,7 +851,9 @@ struct Dec {
             const uint32_t w = __ballot_sync(kFull, (u >> j) & 1u);
             if (lane == 0) sm->dec[row<0>(j) >> 5] = w;
         }
+        tm::wait_st();
         tm::st16(tb + P * PL::L0S, v);
+        push_l0(v);
         nev += 1;
         frontier = N;
         gfr = rank * N + N;
@@ -844,6 +862,7 @@ struct Dec {
         } else {
             xcode = 1;
         }
+        return true;
     }
 
     // PE activations of local stages >= l0 under the final freeze stages
@@ -1066,7 +1085,7 @@ struct Dec {
             // the previous frame is done in both CTAs: reset what the peer writes
             if (rank == 1 && tid == 0) sm->post = 0u;
 #pragma unroll
-            for (int j = 0; j < P; ++j) sm->mb[j][tid] = 0.f;  // the peer's L(1) (init_state: 0)
+            for (int j = 0; j < P; ++j) sm->mb[0][j][tid] = 0.f;  // the peer's L(1) read by sweep 1 (init_state: 0)
             cluster_sync();
             if (rank == 0 && tid == 0) {
                 const unsigned long long idx = atomicAdd(args.queue, 1ull);
@@ -1134,14 +1153,10 @@ struct Dec {
                 it = t;
                 asm volatile("" : "+r"(tid));
                 cross_stage();
-                cluster_arrive();  // this CTA consumed its mailbox
                 nowait = false;
-                if (owner()) {
-                    xcode = 0;
-                    cross_check();
-                    post<0>();  // (first CTA) its frontier after the frame's stage-0 check
-                }
-                cluster_wait();  // so did the peer: L(1) of this sweep may go to it
+                x0 = sign_bits();
+                act0 = act;
+                xpend = owner() && !hfz;  // checked with pass 0's candidates
                 if (hfz) {
                     float v[P];
                     tm::ld16(tb + P * PL::L0S, v);
@@ -1160,30 +1175,38 @@ struct Dec {
                 uint32_t word = g << (r0 & 31);
 #pragma unroll
                 for (int o = 1; o < 32 / P; o <<= 1) word |= __shfl_xor_sync(kFull, word, o);
-                if ((r0 & 31) == 0) {
-                    sm->tu[r0 >> 5] = word;
-                    st_peer(peer_addr(&sm->ptu[r0 >> 5]), word);
+                // x = the frame's transform: first half t0 ^ t1, second half t1;
+                // the first CTA sends t0 ^ x_hat0, the second t1 and whether its
+                // half mismatches (t1 != x_hat1): both then decide the same
+                if ((r0 & 31) == 0) sm->tu[r0 >> 5] = word;
+                __syncthreads();
+                const int gs = it & 1;
+                bool mm1 = false;
+                if (tid < NW) {
+                    const uint32_t t = sm->tu[tid];
+                    st_peer(peer_addr(&sm->gx[gs][tid]), rank == 0 ? t ^ sm->xh[tid] : t);
+                    mm1 = rank == 1 && t != sm->xh[tid];
                 }
-                if (tid < NW) st_peer(peer_addr(&sm->pxh[tid]), sm->xh[tid]);
+                mm1 = __syncthreads_or(mm1);
                 if (tid == 0) {
-                    st_peer(peer_addr(&sm->pst[0]), gfr);
-                    st_peer(peer_addr(&sm->pst[1]), cut);
+                    st_peer(peer_addr(&sm->pst[gs][0]), gfr);
+                    st_peer(peer_addr(&sm->pst[gs][1]), cut);
+                    st_peer(peer_addr(&sm->pst[gs][2]), (int)mm1);
                 }
                 cluster_sync();
-                const int pg = sm->pst[0];
-                if (rank == 0) cut = sm->pst[1];
+                const int pg = sm->pst[gs][0];
+                if (rank == 0) {
+                    cut = sm->pst[gs][1];
+                    mm1 = sm->pst[gs][2] != 0;
+                }
                 gfr = max(gfr, pg);
                 if (gfr < N2) {
-                    // x = the frame's transform: first half t0 ^ t1, second half t1
                     bool mm = false;
                     if (tid < NW) {
-                        const uint32_t t0 = rank == 0 ? sm->tu[tid] : sm->ptu[tid];
-                        const uint32_t t1 = rank == 0 ? sm->ptu[tid] : sm->tu[tid];
-                        const uint32_t h0 = rank == 0 ? sm->xh[tid] : sm->pxh[tid];
-                        const uint32_t h1 = rank == 0 ? sm->pxh[tid] : sm->xh[tid];
-                        mm = ((t0 ^ t1) != h0) || (t1 != h1);
+                        const uint32_t g = sm->gx[gs][tid];
+                        mm = rank == 0 ? ((sm->tu[tid] ^ g) != sm->xh[tid]) : ((g ^ sm->tu[tid]) != 0u);
                     }
-                    converged = !__syncthreads_or(mm);
+                    converged = !__syncthreads_or(mm || mm1);
                 }
             }
             const int stop = (gfr >= N2) ? 2 : (converged ? 1 : 0);
@@ -1348,6 +1371,7 @@ static cudaError_t launch_pair(const DecodeArgs& a, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         if (nc < 1) return cudaErrorInvalidConfiguration;
         max_clusters = nc;
+        if (getenv("PBP_PAIR_INFO")) fprintf(stderr, "pbp: bp_pair_kernel %zu B shared/CTA, %d resident clusters\n", smem, nc);
     }
     long long ncl = std::min<long long>(max_clusters, a.frames);
     if (const char* gc = getenv("PBP_GRID_CAP")) ncl = std::max(1ll, std::min(ncl, atoll(gc) / 2));  // experiments
