@@ -107,6 +107,20 @@ struct Cfg<13, true> {  // half of n = 16384: 512 x 16, one CTA per SM; inner le
     static constexpr int where(int s) { return s == 13 ? kBits : (s <= 3) ? kReg : (s % 4 == 0) ? kSmem : kTmem; }
 };
 
+template <>
+struct Cfg<11, true> {  // half of n = 4096 (A/B experiment, PBP_PAIR=2): the n = 2048 layout, L(1) of the frame in registers
+    static constexpr int LOGT = 7, K = 4, MINB = 2;
+    static constexpr bool r0reg = false, rx2 = false;
+    static constexpr int TMEM_COLS = 0;
+    static constexpr bool L0REG = true;
+    static constexpr int where(int s) { return s == 11 ? kBits : (s <= 3 || s == 5) ? kReg : kSmem; }
+};
+
+template <class C, typename = void>
+struct L0Reg { static constexpr bool value = false; };
+template <class C>
+struct L0Reg<C, std::void_t<decltype(C::L0REG)>> { static constexpr bool value = C::L0REG; };
+
 template <int M_, bool SP_ = false>
 struct Plan {
     using C = Cfg<M_, SP_>;
@@ -138,11 +152,14 @@ struct Plan {
     // TMEM: each warp owns TMEM_COLS * 4 / NWARP columns of its lane quarter, P per level
     static constexpr int TM_WCOLS = C::TMEM_COLS > 0 ? C::TMEM_COLS * 4 / NWARP : 0;
     // SP: the frame's L(1) (local L(0), thread-private in pass 0's layout) in TMEM slot NTM
+    // (L0T), else in registers
+    static constexpr bool L0T = SP && !L0Reg<C>::value;
     static constexpr int L0S = NTM;
+    static constexpr bool TMEM = NTM > 0 || L0T;
     static constexpr bool tm_ok() {
         for (int s = 1; s <= M; ++s)
             if (C::where(s) == kTmem && !(s < M && s / K == (s - 1) / K)) return false;  // inner levels only
-        return (NTM + (SP ? 1 : 0)) * P <= TM_WCOLS || (NTM == 0 && !SP);
+        return (NTM + (L0T ? 1 : 0)) * P <= TM_WCOLS || !TMEM;
     }
     static_assert(tm_ok(), "TMEM levels: thread-private (inner) levels that fit the warp's columns");
     static constexpr int pad(int row) { return row + (row >> 5); }
@@ -280,6 +297,7 @@ struct Dec {
     bool xpend;     // the frame's stage-0 check of this sweep is pending (decided with pass 0's checks)
     uint32_t x0;    // its hard decisions: sign bits of R(1) of this half (pass 0's layout)
     unsigned act0;  // PE activations before this sweep's local stages
+    float l0r[SP && !PL::L0T ? P : 1];  // the frame's L(1) of this half when not in TMEM
     uint32_t rsm;   // the peer's shared memory (cluster window address of its Smem)
 
     // the frame's frontier lies in this half: its candidate blocks are checked here
@@ -453,7 +471,12 @@ struct Dec {
             ++k;
         }
         if constexpr (l0out) {
-            tm::st16(tb + P * PL::L0S, to);
+            if constexpr (PL::L0T) {
+                tm::st16(tb + P * PL::L0S, to);
+            } else {
+#pragma unroll
+                for (int j = 0; j < P; ++j) l0r[j] = to[j];
+            }
             push_l0(to);
         } else if constexpr (tout) {
             tm::st16(tb + P * PL::slot(S), to);
@@ -799,9 +822,14 @@ struct Dec {
     // half to sm->xh (bp_core.cpp:99); its PEs are counted by the first CTA.
     __device__ __forceinline__ void cross_stage() {
         float lo[P];
-        tm::wait_st();
-        tm::ld16(tb + P * PL::L0S, lo);
-        tm::wait_ld();
+        if constexpr (PL::L0T) {
+            tm::wait_st();
+            tm::ld16(tb + P * PL::L0S, lo);
+            tm::wait_ld();
+        } else {
+#pragma unroll
+            for (int j = 0; j < P; ++j) lo[j] = l0r[j];
+        }
         const float* own = llr + (long long)rank * N;
         const float* oth = llr + (long long)(rank ^ 1) * N;
 #pragma unroll
@@ -851,8 +879,13 @@ struct Dec {
             const uint32_t w = __ballot_sync(kFull, (u >> j) & 1u);
             if (lane == 0) sm->dec[row<0>(j) >> 5] = w;
         }
-        tm::wait_st();
-        tm::st16(tb + P * PL::L0S, v);
+        if constexpr (PL::L0T) {
+            tm::wait_st();
+            tm::st16(tb + P * PL::L0S, v);
+        } else {
+#pragma unroll
+            for (int j = 0; j < P; ++j) l0r[j] = v[j];
+        }
         push_l0(v);
         nev += 1;
         frontier = N;
@@ -1131,7 +1164,10 @@ struct Dec {
                     tm::st16(tb + P * k, z);
                     tprot(k) = 0u;
                 }
-                tm::st16(tb + P * PL::L0S, z);
+                if constexpr (PL::L0T) tm::st16(tb + P * PL::L0S, z);
+                else
+#pragma unroll
+                    for (int j = 0; j < P; ++j) l0r[j] = 0.f;
             }
             for (int r = tid; r < N; r += kT) sm->fst[r] = kNotFrozen;
             for (int w = tid; w < NW; w += kT) sm->dec[w] = 0u;
@@ -1159,8 +1195,13 @@ struct Dec {
                 xpend = owner() && !hfz;  // checked with pass 0's candidates
                 if (hfz) {
                     float v[P];
-                    tm::ld16(tb + P * PL::L0S, v);
-                    tm::wait_ld();
+                    if constexpr (PL::L0T) {
+                        tm::ld16(tb + P * PL::L0S, v);
+                        tm::wait_ld();
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < P; ++j) v[j] = l0r[j];
+                    }
                     push_l0(v);
                 } else {
                     sweep_from<0>();
@@ -1274,23 +1315,28 @@ struct Dec {
 
 // SP kernel: a 2-CTA cluster per frame of length 2^(M+1), each CTA one half
 template <int M, int KIND>
-__global__ void __launch_bounds__(Plan<M, true>::T, 1) bp_pair_kernel(const __grid_constant__ DecodeArgs a) {
+__global__ void __launch_bounds__(Plan<M, true>::T, Cfg<M, true>::MINB) bp_pair_kernel(const __grid_constant__ DecodeArgs a) {
     extern __shared__ __align__(16) unsigned char csm[];
     using PL = Plan<M, true>;
     Dec<M, KIND, false, true> dec;
     Smem<M, true>* sm = reinterpret_cast<Smem<M, true>*>(csm);
-    constexpr int COLS = Cfg<M, true>::TMEM_COLS;
-    const int warp = threadIdx.x >> 5;
-    if (warp == 0) tm::alloc<COLS>(&sm->tbase);
-    tm::fence_before();
-    __syncthreads();
-    tm::fence_after();
-    dec.tb = sm->tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(PL::TM_WCOLS * (warp >> 2));
-    dec.run_pair(a, sm);
-    tm::fence_before();
-    __syncthreads();
-    tm::fence_after();
-    if (warp == 0) tm::dealloc<COLS>(sm->tbase);
+    if constexpr (PL::TMEM) {
+        constexpr int COLS = Cfg<M, true>::TMEM_COLS;
+        const int warp = threadIdx.x >> 5;
+        if (warp == 0) tm::alloc<COLS>(&sm->tbase);
+        tm::fence_before();
+        __syncthreads();
+        tm::fence_after();
+        dec.tb = sm->tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(PL::TM_WCOLS * (warp >> 2));
+        dec.run_pair(a, sm);
+        tm::fence_before();
+        __syncthreads();
+        tm::fence_after();
+        if (warp == 0) tm::dealloc<COLS>(sm->tbase);
+    } else {
+        dec.tb = 0;
+        dec.run_pair(a, sm);
+    }
 }
 
 template <int M, int KIND, bool XH = false>
@@ -1365,7 +1411,7 @@ static cudaError_t launch_pair(const DecodeArgs& a, cudaStream_t st) {
     cfg.numAttrs = 1;
     static int max_clusters = 0;  // per process (one device model)
     if (!max_clusters) {
-        cfg.gridDim = dim3(2 * 74);
+        cfg.gridDim = dim3(2 * 148 * 4);
         int nc = 0;
         e = cudaOccupancyMaxActiveClusters(&nc, k, &cfg);
         if (e != cudaSuccess) return e;
@@ -1415,13 +1461,27 @@ long long cta_scratch_floats(int m) {
 // frame per SM: every message level on chip (PBP_PAIR=0: one CTA per frame)
 bool cta_pair_on(int m, int kind) {
     const char* e = getenv("PBP_PAIR");  // read per launch: tests compare both layouts in one process
-    return (e ? atoi(e) : 1) && m == 14 && kind == 2;
+    const int v = e ? atoi(e) : 1;
+    // n = 4096 on pairs only as an experiment (PBP_PAIR=2): slower, see DESIGN.md section 5
+    return kind == 2 && ((v && m == 14) || (v >= 2 && m == 12));
 }
 static bool cta_pair(const DecodeArgs& a) { return cta_pair_on(a.m, a.kind) && !a.events && !a.ev_xhat; }
-size_t cta_pair_smem_bytes() { return sizeof(cta::Smem<13, true>); }
+template <int M>
+static int pair_occ() {
+    auto k = cta::bp_pair_kernel<M, 2>;
+    const size_t smem = sizeof(cta::Smem<M, true>);
+    int nb = 0;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, cta::Plan<M, true>::T, smem) != cudaSuccess) return 0;
+    return nb;
+}
+int cta_pair_warps_per_sm(int m) {
+    return m == 12 ? pair_occ<11>() * cta::Plan<11, true>::NWARP : pair_occ<13>() * cta::Plan<13, true>::NWARP;
+}
+size_t cta_pair_smem_bytes(int m) { return m == 12 ? sizeof(cta::Smem<11, true>) : sizeof(cta::Smem<13, true>); }
 
 cudaError_t launch_cta(const DecodeArgs& a, int grid, cudaStream_t st) {
-    if (cta_pair(a)) return cta::launch_pair<13, 2>(a, st);
+    if (cta_pair(a)) return a.m == 14 ? cta::launch_pair<13, 2>(a, st) : cta::launch_pair<11, 2>(a, st);
     switch (a.m) {
         case 11: return cta::launch_m<11>(a, grid, st);
         case 12: return cta::launch_m<12>(a, grid, st);

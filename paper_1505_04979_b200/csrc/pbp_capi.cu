@@ -33,7 +33,8 @@ int cta_blocks_per_sm(int m, int kind);
 size_t cta_smem_bytes(int m);
 int cta_warps(int m);
 bool cta_pair_on(int m, int kind);
-size_t cta_pair_smem_bytes();
+size_t cta_pair_smem_bytes(int m);
+int cta_pair_warps_per_sm(int m);
 cudaError_t launch_channel(const GenArgs& g, int grid, cudaStream_t stream);
 long long channel_seed_words(long long count);
 }  // namespace pbp
@@ -563,8 +564,8 @@ int pbp_kernel_info(int32_t n, int decoder, int32_t* smem_bytes, int32_t* warps_
         if (smem_bytes) *smem_bytes = (int32_t)pbp::warp_smem_bytes(m, decoder);
         if (warps_per_sm) *warps_per_sm = pbp::warp_blocks_per_sm(m, decoder) * pbp::warp_kernel_warps(m);
     } else if (pbp::cta_pair_on(m, decoder)) {  // half a frame per CTA (2-CTA clusters), one CTA per SM
-        if (smem_bytes) *smem_bytes = (int32_t)pbp::cta_pair_smem_bytes();
-        if (warps_per_sm) *warps_per_sm = pbp_device_count() > 0 ? 16 : 0;
+        if (smem_bytes) *smem_bytes = (int32_t)pbp::cta_pair_smem_bytes(m);
+        if (warps_per_sm) *warps_per_sm = pbp_device_count() > 0 ? pbp::cta_pair_warps_per_sm(m) : 0;
     } else if (pbp::cta_kernel_supported(m)) {  // CTA per frame: shared bytes per CTA, resident warps
         if (smem_bytes) *smem_bytes = (int32_t)pbp::cta_smem_bytes(m);
         if (warps_per_sm) *warps_per_sm = pbp::cta_blocks_per_sm(m, decoder) * pbp::cta_warps(m);

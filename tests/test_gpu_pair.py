@@ -156,3 +156,23 @@ def test_pair_equals_one_cta_per_frame(ctx, monkeypatch):
             monkeypatch.setenv("PBP_PAIR", on)
             cnts.append(P.simulate_point(code, "csfg", 5, 0, 2000, snr, 0.9375, 40, ctx=ctx))
         assert cnts[0] == cnts[1], snr
+
+
+@pytest.mark.parametrize("snr", [2.5, 4.0, 6.0])
+def test_pair_n4096_experiment(ctx, monkeypatch, snr):
+    """The n = 4096 pair layout (PBP_PAIR=2, an A/B experiment: each CTA holds half of
+    the frame in the n = 2048 layout, L(1) of the frame in registers) against the
+    oracle and the default layout."""
+    n = 4096
+    monkeypatch.setenv("PBP_PAIR", "2")
+    assert P.lib.pbp_kernel_cluster(n, 2) == 2
+    k = n // 2 if snr < 6.0 else 3 * n // 4
+    fz = O.construct(n, k, Z0)
+    _, llr64 = O.trials(4, 0, 24, fz, snr, lib=O.C)
+    llr = llr64.astype(np.float32)
+    exp = O.decode_batch("csfg", fz, llr, 0.9375, 60, prec=32)
+    got = P.decode_batch(P.PolarCode.from_frozen_mask(n, fz), "csfg", llr, 0.9375, 60, ctx=ctx)
+    u = P.unpack_bits(got["u_hat_bits"], n)
+    assert np.array_equal(u, exp["u_hat"])
+    for f in ("iterations", "pe", "stop", "n_events"):
+        assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), f

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--max-iter", type=int, default=40)
     ap.add_argument("--seed", type=int, default=5)
+    ap.add_argument("--on", default="1", help="PBP_PAIR value of the pair arm (2: also n = 4096)")
     a = ap.parse_args()
     n = a.n
     ctx = P.Context(0)
@@ -39,7 +40,7 @@ def main():
         stream.synchronize()
         res = {}
         for rep in range(a.reps):
-            for on in ("1", "0"):
+            for on in (a.on, "0"):
                 os.environ["PBP_PAIR"] = on
                 cnt = torch.zeros(10, dtype=torch.int64, device=dev)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -53,7 +54,7 @@ def main():
                 c = cnt.tolist()
                 if rep == a.reps - 1 or on not in res:
                     res[on] = (ms, c)
-        (m1, c1), (m0, c0) = res["1"], res["0"]
+        (m1, c1), (m0, c0) = res[a.on], res["0"]
         print(json.dumps({"n": n, "ebn0_db": snr, "frames": a.frames, "pair_ms": round(m1, 3), "cta_ms": round(m0, 3),
                           "speedup": round(m0 / m1, 3), "counters_equal": c1 == c0,
                           "pair_roofline_frac": round(c1[5] / (m1 / 1e3) / peak_pe, 4),
