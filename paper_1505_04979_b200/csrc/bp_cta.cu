@@ -62,6 +62,20 @@ struct Cfg<11> {  // 128 threads x 16 rows, 3 CTAs per SM: four levels in regist
     static constexpr int where(int s) { return s == 11 ? kBits : (s <= 3 || s == 5) ? kReg : kSmem; }
 };
 template <>
+struct Cfg<12> {  // 256 x 16, two frames per SM, every level on chip: four in registers, two in shared memory, five in TMEM
+    static constexpr int LOGT = 8, K = 4, MINB = 2;
+    static constexpr bool r0reg = false, rx2 = false;
+    // 256 columns per CTA: two CTAs per SM share the 512 (the occupancy API reports one
+    // CTA per SM for a kernel that allocates TMEM; a grid of two per SM co-resides:
+    // cta_blocks_per_sm). Against levels 6..9 in shared memory and 10, 11 in L2: +3 %.
+    static constexpr int TMEM_COLS = 256;
+    static constexpr bool TPROT_REG = false;
+    static constexpr int where(int s) {
+        return s == 12 ? kBits : (s <= 3 || s == 5) ? kReg : (s == 4 || s == 8) ? kSmem : kTmem;
+    }
+};
+#if 0  // round-1 layout (two levels in L2)
+template <>
 struct Cfg<12> {  // 256 x 16, two frames per SM: four levels in registers, five in shared memory, two in L2
     static constexpr int LOGT = 8, K = 4, MINB = 2;
     static constexpr bool r0reg = false, rx2 = false;
@@ -72,6 +86,7 @@ struct Cfg<12> {  // 256 x 16, two frames per SM: four levels in registers, five
         return s == 12 ? kBits : (s <= 3 || s == 5) ? kReg : (s == 10 || s == 11) ? kGlob : kSmem;
     }
 };
+#endif
 template <>
 struct Cfg<13> {  // 512 x 16: three levels in registers, three in shared memory, six in TMEM (all on chip)
     static constexpr int LOGT = 9, K = 4, MINB = 1;
@@ -1439,7 +1454,15 @@ static int occ_t() {
 
 template <int M>
 static int occ_m(int kind) {
-    return kind == 0 ? occ_t<M, 0>() : kind == 1 ? occ_t<M, 1>() : occ_t<M, 2>();
+    const int nb = kind == 0 ? occ_t<M, 0>() : kind == 1 ? occ_t<M, 1>() : occ_t<M, 2>();
+    if constexpr (Plan<M>::TMEM) {
+        // the occupancy API counts one CTA per SM for a kernel that allocates tensor
+        // memory; CTAs whose columns fit the SM's 512 together do co-reside
+        static_assert(Cfg<M>::MINB * Cfg<M>::TMEM_COLS <= 512, "TMEM columns of the resident CTAs");
+        static_assert(Cfg<M>::MINB * (sizeof(Smem<M>) + 1024) <= 228 * 1024, "shared memory of the resident CTAs");
+        return nb > 0 ? std::max(nb, (int)Cfg<M>::MINB) : 0;
+    }
+    return nb;
 }
 
 }  // namespace cta
