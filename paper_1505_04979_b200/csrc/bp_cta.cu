@@ -169,12 +169,13 @@ struct Plan {
     // SP: the frame's L(1) (local L(0), thread-private in pass 0's layout) in TMEM slot NTM
     // (L0T), else in registers
     static constexpr bool L0T = SP && !L0Reg<C>::value;
-    static constexpr int L0S = NTM;
+    // (with L0T, this half's R(0) in TMEM slot NTM + 1)
+    static constexpr int L0S = NTM, R0S = NTM + 1;
     static constexpr bool TMEM = NTM > 0 || L0T;
     static constexpr bool tm_ok() {
         for (int s = 1; s <= M; ++s)
             if (C::where(s) == kTmem && !(s < M && s / K == (s - 1) / K)) return false;  // inner levels only
-        return (NTM + (L0T ? 1 : 0)) * P <= TM_WCOLS || !TMEM;
+        return (NTM + (L0T ? 2 : 0)) * P <= TM_WCOLS || !TMEM;
     }
     static_assert(tm_ok(), "TMEM levels: thread-private (inner) levels that fit the warp's columns");
     static constexpr int pad(int row) { return row + (row >> 5); }
@@ -263,7 +264,9 @@ struct Smem {
     uint32_t tbase;                                // TMEM allocation
     // SP: what the peer CTA of the pair writes here (st.shared::cluster)
     // double-buffered by iteration parity: the peer writes sweep t's while this CTA may still read t-1's
-    float mb[SP ? 2 : 1][SP ? PL::P : 1][SP ? PL::T : 1];  // the peer's half of L(1) (its local L(0)), pass-0 thread positions
+    // the peer's stage-0 term at pass-0 thread positions: from the first CTA
+    // alpha * min-with-sign(L(1), R(0)) (the PE's cross term), from the second L(1) + R(0)
+    float mb[SP ? 2 : 1][SP ? PL::P : 1][SP ? PL::T : 1];
     uint32_t gx[SP ? 2 : 1][SP ? PL::NW : 1];     // G-check words from the peer (first CTA: t1; second: t0 ^ x_hat0)
     int pst[2][4];                                 // the peer's frontier (global), completion stage, mismatch of its half
     long long pfin[3];                             // frame end (from the second CTA): bit errors, PEs, events
@@ -491,8 +494,7 @@ struct Dec {
             } else {
 #pragma unroll
                 for (int j = 0; j < P; ++j) l0r[j] = to[j];
-            }
-            push_l0(to);
+            }  // (pushed to the peer after the sweep: push_l1)
         } else if constexpr (tout) {
             tm::st16(tb + P * PL::slot(S), to);
         }
@@ -788,10 +790,44 @@ struct Dec {
     // block is smaller) -- then it stops waiting until the next sweep.
     // After the frontier crossed, neither waits.
 
-    // local L(0) of this sweep (the frame's L(1)) into the peer's mailbox
-    __device__ __forceinline__ void push_l0(const float* v) const {
+    // this half's R(0) (pass 0's layout, -0 -> +0)
+    __device__ __forceinline__ void own_r0(float (&r)[P]) const {
+        if constexpr (PL::L0T) {
+            tm::ld16(tb + P * PL::R0S, r);
+            tm::wait_ld();
+        } else {
 #pragma unroll
-        for (int j = 0; j < P; ++j) st_peer(peer_addr(&sm->mb[it & 1][j][tid]), v[j]);
+            for (int j = 0; j < P; ++j) r[j] = __fadd_rn(llr[(long long)rank * N + row<0>(j)], 0.0f);
+        }
+    }
+
+    // The frame's stage-0 term the peer needs from this half's L(1) = v (local
+    // L(0) of this sweep) and R(0), into its mailbox: the first CTA sends the
+    // cross term alpha * min-with-sign(L(1), R(0)), the second L(1) + R(0)
+    // (bp_core.cpp:21-24: the same operations on the same operands as a
+    // one-CTA stage 0, so the peer needs no R(0) of this half)
+    // this sweep's L(1) of the half (local stage 0's output, or +-CAP once frozen)
+    __device__ __forceinline__ void push_l1() const {
+        float v[P];
+        if constexpr (PL::L0T) {
+            tm::wait_st();
+            tm::ld16(tb + P * PL::L0S, v);
+            tm::wait_ld();
+        } else {
+#pragma unroll
+            for (int j = 0; j < P; ++j) v[j] = l0r[j];
+        }
+        push_x(v);
+    }
+
+    __device__ __forceinline__ void push_x(const float* v) const {
+        float r[P];
+        own_r0(r);
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            const float x = rank == 0 ? __fmul_rn(alpha, xsmin(v[j], r[j])) : __fadd_rn(v[j], r[j]);
+            st_peer(peer_addr(&sm->mb[it & 1][j][tid]), x);
+        }
     }
 
     template <int PH>
@@ -836,39 +872,33 @@ struct Dec {
     // this half goes to R (pass 0's layout), x_hat = (R(0) + L(0) < 0) of this
     // half to sm->xh (bp_core.cpp:99); its PEs are counted by the first CTA.
     __device__ __forceinline__ void cross_stage() {
-        float lo[P];
+        float lo[P], r0[P];
         if constexpr (PL::L0T) {
             tm::wait_st();
             tm::ld16(tb + P * PL::L0S, lo);
-            tm::wait_ld();
         } else {
 #pragma unroll
             for (int j = 0; j < P; ++j) lo[j] = l0r[j];
         }
-        const float* own = llr + (long long)rank * N;
-        const float* oth = llr + (long long)(rank ^ 1) * N;
+        own_r0(r0);
 #pragma unroll
         for (int j = 0; j < P; ++j) {
-            const int r = row<0>(j);
-            const float mine = __fadd_rn(own[r], 0.0f), peer = __fadd_rn(oth[r], 0.0f);
-            const float lp = sm->mb[(it - 1) & 1][j][tid];
-            const float lt = rank == 0 ? lo[j] : lp, lb = rank == 0 ? lp : lo[j];
-            const float r_t = rank == 0 ? mine : peer, r_b = rank == 0 ? peer : mine;
-            const float cross = __fmul_rn(alpha, xsmin(lt, r_t));
-            const float sum_bot = __fadd_rn(lb, r_b);
+            // the first CTA: l_top and R(1) of the top rows from the peer's L(1) + R(0)
+            // (sum_bot); the second: l_bot and R(1) of the bottom rows from the cross term
+            const float pm = sm->mb[(it - 1) & 1][j][tid];
             float rn, x;
             if (rank == 0) {
-                const float l_top = __fmul_rn(alpha, xsmin(lt, sum_bot));
-                rn = __fmaf_rn(alpha, xsmin(r_t, sum_bot), 0.0f);
-                x = __fadd_rn(r_t, l_top);
+                const float l_top = __fmul_rn(alpha, xsmin(lo[j], pm));
+                rn = __fmaf_rn(alpha, xsmin(r0[j], pm), 0.0f);
+                x = __fadd_rn(r0[j], l_top);
             } else {
-                const float l_bot = __fadd_rn(lb, cross);
-                rn = __fadd_rn(r_b, cross);
-                x = __fadd_rn(r_b, l_bot);
+                const float l_bot = __fadd_rn(lo[j], pm);
+                rn = __fadd_rn(r0[j], pm);
+                x = __fadd_rn(r0[j], l_bot);
             }
             R[j] = rn;
             const uint32_t w = __ballot_sync(kFull, x < 0.f);
-            if (lane == 0) sm->xh[r >> 5] = w;
+            if (lane == 0) sm->xh[row<0>(j) >> 5] = w;
         }
         if (rank == 0) act += P;
     }
@@ -901,7 +931,6 @@ struct Dec {
 #pragma unroll
             for (int j = 0; j < P; ++j) l0r[j] = v[j];
         }
-        push_l0(v);
         nev += 1;
         frontier = N;
         gfr = rank * N + N;
@@ -1132,8 +1161,6 @@ struct Dec {
         for (;;) {
             // the previous frame is done in both CTAs: reset what the peer writes
             if (rank == 1 && tid == 0) sm->post = 0u;
-#pragma unroll
-            for (int j = 0; j < P; ++j) sm->mb[0][j][tid] = 0.f;  // the peer's L(1) read by sweep 1 (init_state: 0)
             cluster_sync();
             if (rank == 0 && tid == 0) {
                 const unsigned long long idx = atomicAdd(args.queue, 1ull);
@@ -1179,10 +1206,20 @@ struct Dec {
                     tm::st16(tb + P * k, z);
                     tprot(k) = 0u;
                 }
-                if constexpr (PL::L0T) tm::st16(tb + P * PL::L0S, z);
-                else
+                if constexpr (PL::L0T) {
+                    tm::st16(tb + P * PL::L0S, z);
+                    float r[P];
+#pragma unroll
+                    for (int j = 0; j < P; ++j) r[j] = __fadd_rn(llr[(long long)rank * N + row<0>(j)], 0.0f);
+                    tm::st16(tb + P * PL::R0S, r);
+                } else {
 #pragma unroll
                     for (int j = 0; j < P; ++j) l0r[j] = 0.f;
+                }
+                tm::wait_st();
+                // sweep 1's stage-0 terms (L(1) = 0) into the peer's mailbox slot 0
+                it = 0;
+                push_x(z);
             }
             for (int r = tid; r < N; r += kT) sm->fst[r] = kNotFrozen;
             for (int w = tid; w < NW; w += kT) sm->dec[w] = 0u;
@@ -1195,7 +1232,7 @@ struct Dec {
             ph = 0;
             if (tid < 3) sm->vw[tid] = 0u;
             act = 0;
-            __syncthreads();
+            cluster_sync();  // (and the peer's sweep-1 terms are in the mailbox)
             int iters = 0;
             bool converged = false;
             for (int t = 1; t <= args.max_iter; ++t) {
@@ -1208,20 +1245,11 @@ struct Dec {
                 x0 = sign_bits();
                 act0 = act;
                 xpend = owner() && !hfz;  // checked with pass 0's candidates
-                if (hfz) {
-                    float v[P];
-                    if constexpr (PL::L0T) {
-                        tm::ld16(tb + P * PL::L0S, v);
-                        tm::wait_ld();
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < P; ++j) v[j] = l0r[j];
-                    }
-                    push_l0(v);
-                } else {
+                if (!hfz) {
                     sweep_from<0>();
                     if constexpr (PL::NTM > 0) fixup_tmem();
                 }
+                push_l1();
                 // pinned G-check inputs: this half's hard output (rows < frontier
                 // from decided_u), transformed over the half's row bits
                 uint32_t g = bits_transform<K>(u_group(frontier));
