@@ -305,6 +305,7 @@ struct Dec {
     FzT snap;      // sign bits of R(S+1) after each stage of the current pass
     uint32_t onm;  // PE activations of the current pass, bit i * P/2 + k
     unsigned act;  // this thread's PE activations (< 2^32 per frame)
+    bool ownp;     // this warp holds rows of a candidate block of the current pass (warp-uniform)
     // SP (one half of a frame on a 2-CTA cluster)
     int rank;       // 0: the frame's rows [0, N), 1: rows [N, 2N)
     int gfr;        // the frame's frontier, 0 .. 2N (frontier = this half's part of it)
@@ -398,6 +399,25 @@ struct Dec {
     // the stage loop, csfg_freeze.cpp:109). csfg checks are deferred to the
     // end of the pass (pass_check): the pass's stages run as if no check of
     // the pass commits, and the commits correct that afterwards.
+    // Can this warp hold rows of a candidate block of pass q? Every frontier the
+    // pass can reach lies in [f0, fend], fend = the end of f0's block at the
+    // pass's first stage (later blocks nest inside it), and a candidate block of
+    // the pass lies in the rows whose bits >= b + K are those of its frontier:
+    // threads tid >> b = f0 >> (b + K) or fend >> (b + K), at most two warps when
+    // b <= 5. With b > 5 the warp transform needs every warp.
+    template <int q>
+    __device__ __forceinline__ bool own_pass() const {
+        constexpr int b = PL::base(q);
+        if constexpr (b > 5) {
+            return true;
+        } else {
+            const int f0 = frontier;
+            const int fend = ((f0 >> (b + K - 1)) + 1) << (b + K - 1);
+            const int th = tid >> b;
+            return __any_sync(kFull, th == (f0 >> (b + K)) || th == (fend >> (b + K)));
+        }
+    }
+
     template <int S>
     __device__ __forceinline__ bool stage() {
         constexpr int q = PL::pass_of(S);
@@ -410,6 +430,7 @@ struct Dec {
             if constexpr (i == 0) {
                 snap = 0;
                 onm = 0u;
+                ownp = own_pass<q>();
             }
         }
         float lt[P / 2], lb[P / 2];
@@ -501,7 +522,7 @@ struct Dec {
         act += __popc(onb);
         if constexpr (csfg) {
             onm |= onb << (i * (P / 2));
-            snap |= (FzT)sign_bits() << (i * P);
+            if (ownp) snap |= (FzT)sign_bits() << (i * P);
         }
         constexpr bool pass_end = S == PL::last(q);
         constexpr bool boundary = pass_end && q + 1 < Q;
@@ -641,15 +662,19 @@ struct Dec {
             }
             xcode = 0;
         }
-        FzT W = pass_bits<q, 0>();
-        W = lane_transform<(b < 5 ? b : 5)>(W);
-        if constexpr (b > 5) W = warp_transform<b - 5>(W);
-        int f[(1 << nst) - 1 + (1 << nst)];
-        f[0] = frontier;
-        uint32_t bad = pass_viol<q, 0>(W, f);
-        bad = __reduce_or_sync(kFull, bad);
-        if (lane == 0 && bad) atomicOr(&sm->vw[ph], bad);
+        FzT W = 0;
+        if (ownp) {  // (warps without rows of a candidate contribute no violation)
+            W = pass_bits<q, 0>();
+            W = lane_transform<(b < 5 ? b : 5)>(W);
+            if constexpr (b > 5) W = warp_transform<b - 5>(W);
+            int f[(1 << nst) - 1 + (1 << nst)];
+            f[0] = frontier;
+            uint32_t bad = pass_viol<q, 0>(W, f);
+            bad = __reduce_or_sync(kFull, bad);
+            if (lane == 0 && bad) atomicOr(&sm->vw[ph], bad);
+        }
         __syncthreads();
+        uint32_t bad;
         bad = sm->vw[ph];
         if (tid == 0) sm->vw[ph == 0 ? 2 : ph - 1] = 0u;  // used two checks from now
         ph = ph == 2 ? 0 : ph + 1;
