@@ -70,6 +70,7 @@ struct Cfg<12> {  // 256 x 16, two frames per SM, every level on chip: four in r
     // cta_blocks_per_sm). Against levels 6..9 in shared memory and 10, 11 in L2: +3 %.
     static constexpr int TMEM_COLS = 256;
     static constexpr bool TPROT_REG = false;
+    static constexpr bool PACK(int kind) { return kind != 2; }
     static constexpr int where(int s) {
         return s == 12 ? kBits : (s <= 3 || s == 5) ? kReg : (s == 4 || s == 8) ? kSmem : kTmem;
     }
@@ -93,6 +94,7 @@ struct Cfg<13> {  // 512 x 16: three levels in registers, three in shared memory
     static constexpr bool r0reg = false, rx2 = false;
     static constexpr int TMEM_COLS = 512;  // 16 warps: 128 columns of its lane quarter per warp
     static constexpr bool TPROT_REG = false;
+    static constexpr bool PACK(int) { return true; }
     // the inner levels of passes 1 and 2 in TMEM (5 and 6 in shared memory measured 1.8 % slower)
     static constexpr int where(int s) { return s == 13 ? kBits : (s <= 3) ? kReg : (s % 4 == 0) ? kSmem : kTmem; }
 };
@@ -133,6 +135,13 @@ struct Cfg<11, true> {  // half of n = 4096 (A/B experiment, PBP_PAIR=2): the n 
 
 template <class C, typename = void>
 struct L0Reg { static constexpr bool value = false; };
+// packed fp32x2 PE math per layout and decoder (PACK(kind)); scalar where the
+// packed pairs' register pressure spills (measured: n = 8192 +2.5 %, n = 4096
+// G-stop +5.5 %, n = 4096 csfg -0.8 %, the pair -2.9 %, n = 16384 G-stop -10 %)
+template <class C, typename = void>
+struct Pack { static constexpr bool on(int) { return false; } };
+template <class C>
+struct Pack<C, std::void_t<decltype(C::PACK(0))>> { static constexpr bool on(int kind) { return C::PACK(kind); } };
 template <class C>
 struct L0Reg<C, std::void_t<decltype(C::L0REG)>> { static constexpr bool value = C::L0REG; };
 
@@ -189,6 +198,18 @@ __device__ __forceinline__ float xsmin(float a, float b) {
     float d;
     asm("min.xorsign.abs.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
     return d;
+}
+
+// packed fp32x2 arithmetic (FADD2 / FFMA2), round-to-nearest per half
+__device__ __forceinline__ void add2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+    asm("{ .reg .b64 a, b, d; mov.b64 a, {%2, %3}; mov.b64 b, {%4, %5}; add.rn.f32x2 d, a, b; mov.b64 {%0, %1}, d; }"
+        : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+// s * a + (+0): the single-rounded product, never -0
+__device__ __forceinline__ void fma2s0(float& d0, float& d1, float s, float a0, float a1) {
+    asm("{ .reg .b64 a, b, c, d; mov.b64 a, {%2, %2}; mov.b64 b, {%3, %4}; mov.b64 c, 0; "
+        "fma.rn.f32x2 d, a, b, c; mov.b64 {%0, %1}, d; }"
+        : "=f"(d0), "=f"(d1) : "f"(s), "f"(a0), "f"(a1));
 }
 
 // thread-block cluster (SP pair): rank, barrier, distributed shared memory
@@ -468,19 +489,11 @@ struct Dec {
             }
             ++k;
         }
-#pragma unroll
-        for (int j = 0, k = 0; j < P; ++j) {
-            if (j & dj) continue;
-            const int rt = row<q>(j), rb = rt + (1 << g);
-            bool xt = false, xb = false;
-            // every PE is computed; an inactive one keeps R and L unchanged
-            // (selects and predicated stores instead of a branch per PE)
+        // PE outputs of the pair (j, j + dj): stores / selects / stage-0 decisions
+        auto emit = [&](int j, int k, float l_top, float l_bot, float n_t, float n_b) {
             const bool on = (onb >> k) & 1u;
             const float r_t = R[j], r_b = R[j + dj];
-            const float cross = __fmul_rn(alpha, xsmin(lt[k], r_t));
-            const float sum_bot = __fadd_rn(lb[k], r_b);
-            const float l_top = __fmul_rn(alpha, xsmin(lt[k], sum_bot));
-            const float l_bot = __fadd_rn(lb[k], cross);
+            bool xt = false, xb = false;
             if constexpr (tout) {
                 // every PE's outputs (an inactive PE's only matter at a frozen block's
                 // boundary L, which fixup_tmem restores after the sweep)
@@ -495,19 +508,52 @@ struct Dec {
                 xt = __fadd_rn(r_t, l_top) < 0.f;
                 xb = __fadd_rn(r_b, l_bot) < 0.f;
             }
-            const float n_t = __fmaf_rn(alpha, xsmin(r_t, sum_bot), 0.0f);
-            const float n_b = __fadd_rn(r_b, cross);
             R[j] = on ? n_t : r_t;
             R[j + dj] = on ? n_b : r_b;
             if constexpr (S == 0 && KIND != 0 && !SP) {
                 // pass 0: a warp's lanes hold 32 consecutive rows of every register
+                const int rt = row<q>(j), rb = rt + (1 << g);
                 const uint32_t wt = __ballot_sync(kFull, xt), wb = __ballot_sync(kFull, xb);
                 if (lane == 0) {
                     sm->xh[rt >> 5] = wt;
                     sm->xh[rb >> 5] = wb;
                 }
             }
-            ++k;
+        };
+        // every PE is computed; an inactive one keeps R and L unchanged (selects and
+        // predicated stores instead of a branch per PE)
+        if constexpr (dj >= 2 && Pack<C>::on(KIND)) {
+            // two PEs per packed fp32x2 instruction (FADD2 / FFMA2), as the warp
+            // kernel: products as fma(alpha, m, +0) (ptxas would fuse a bare
+            // mul.f32x2 into the following add; the +0 addend only turns a -0
+            // product into +0, which no decision distinguishes)
+#pragma unroll
+            for (int j = 0, k = 0; j < P; j += 2) {
+                if (j & dj) continue;
+                const float r_t0 = R[j], r_t1 = R[j + 1], r_b0 = R[j + dj], r_b1 = R[j + dj + 1];
+                float c0, c1, s0, s1, lt0, lt1, lb0, lb1, nt0, nt1, nb0, nb1;
+                fma2s0(c0, c1, alpha, xsmin(lt[k], r_t0), xsmin(lt[k + 1], r_t1));
+                add2(s0, s1, lb[k], lb[k + 1], r_b0, r_b1);
+                fma2s0(lt0, lt1, alpha, xsmin(lt[k], s0), xsmin(lt[k + 1], s1));
+                add2(lb0, lb1, lb[k], lb[k + 1], c0, c1);
+                fma2s0(nt0, nt1, alpha, xsmin(r_t0, s0), xsmin(r_t1, s1));
+                add2(nb0, nb1, r_b0, r_b1, c0, c1);
+                emit(j, k, lt0, lb0, nt0, nb0);
+                emit(j + 1, k + 1, lt1, lb1, nt1, nb1);
+                k += 2;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0, k = 0; j < P; ++j) {
+                if (j & dj) continue;
+                const float r_t = R[j], r_b = R[j + dj];
+                const float cross = __fmul_rn(alpha, xsmin(lt[k], r_t));
+                const float sum_bot = __fadd_rn(lb[k], r_b);
+                const float l_top = __fmul_rn(alpha, xsmin(lt[k], sum_bot));
+                const float l_bot = __fadd_rn(lb[k], cross);
+                emit(j, k, l_top, l_bot, __fmaf_rn(alpha, xsmin(r_t, sum_bot), 0.0f), __fadd_rn(r_b, cross));
+                ++k;
+            }
         }
         if constexpr (l0out) {
             if constexpr (PL::L0T) {
