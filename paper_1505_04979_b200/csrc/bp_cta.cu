@@ -180,6 +180,9 @@ struct Plan {
     static constexpr bool L0T = SP && !L0Reg<C>::value;
     // (with L0T, this half's R(0) in TMEM slot NTM + 1)
     static constexpr int L0S = NTM, R0S = NTM + 1;
+    // one CTA per frame: R(0) in TMEM slot NTM when a TMEM layout has the columns
+    // (one tcgen05.ld per sweep instead of P global loads)
+    static constexpr bool R0T = !SP && NTM > 0 && (NTM + 1) * P <= TM_WCOLS;
     static constexpr bool TMEM = NTM > 0 || L0T;
     static constexpr bool tm_ok() {
         for (int s = 1; s <= M; ++s)
@@ -1114,6 +1117,11 @@ struct Dec {
                     tm::st16(tb + P * k, z);
                     tprot(k) = 0u;
                 }
+                if constexpr (PL::R0T) {
+#pragma unroll
+                    for (int j = 0; j < P; ++j) z[j] = __fadd_rn(llr[row<0>(j)], 0.0f);
+                    tm::st16(tb + P * PL::NTM, z);
+                }
             }
             for (int r = tid; r < N; r += kT) sm->fst[r] = kNotFrozen;
             for (int w = tid; w < NW; w += kT) sm->dec[w] = 0u;
@@ -1135,10 +1143,16 @@ struct Dec {
                 // keep the per-stage row/address arithmetic inside the loop
                 // (hoisted for every stage it would not fit in the registers)
                 asm volatile("" : "+r"(tid));
+                if constexpr (PL::R0T) {
+                    tm::wait_st();
+                    tm::ld16(tb + P * PL::NTM, R);
+                    tm::wait_ld();
+                } else {
 #pragma unroll
-                for (int j = 0; j < P; ++j) {
-                    if constexpr (C::r0reg) R[j] = R0[j];
-                    else R[j] = __fadd_rn(llr[row<0>(j)], 0.0f);
+                    for (int j = 0; j < P; ++j) {
+                        if constexpr (C::r0reg) R[j] = R0[j];
+                        else R[j] = __fadd_rn(llr[row<0>(j)], 0.0f);
+                    }
                 }
                 sweep_from<0>();
                 if constexpr (csfg && PL::NTM > 0) fixup_tmem();
