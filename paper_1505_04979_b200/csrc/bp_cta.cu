@@ -122,7 +122,7 @@ struct Cfg<14> {  // 1024 x 16: one level in shared memory, four in TMEM, the re
 template <>
 struct Cfg<13, true> {  // half of n = 16384: 512 x 16, one CTA per SM; inner levels 5..11 in TMEM, L(1) of the frame too
     static constexpr int LOGT = 9, K = 4, MINB = 1;
-    static constexpr bool r0reg = false, rx2 = true;
+    static constexpr bool r0reg = false, rx2 = false;
     static constexpr int TMEM_COLS = 512;  // 16 warps: 128 columns per warp = six levels + L(1) of the frame
     static constexpr bool TPROT_REG = false;
     static constexpr int where(int s) { return s == 13 ? kBits : (s <= 3) ? kReg : (s % 4 == 0) ? kSmem : kTmem; }
@@ -252,11 +252,6 @@ __device__ __forceinline__ void st_peer(uint32_t addr, long long v) {
 __device__ __forceinline__ void st_peer(uint32_t addr, unsigned long long v) {
     asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }
-__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
-    return v;
-}
 __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
@@ -296,15 +291,14 @@ struct Smem {
     uint32_t tprot[(PL::NTM > 0 && !TprotReg<C>::value) ? PL::NTM : 1][(PL::NTM > 0 && !TprotReg<C>::value) ? PL::T : 1];
     uint32_t tbase;                                // TMEM allocation
     // SP: what the peer CTA of the pair writes here (st.shared::cluster)
+    // double-buffered by iteration parity: the peer writes sweep t's while this CTA may still read t-1's
     // the peer's stage-0 term at pass-0 thread positions: from the first CTA
-    // alpha * min-with-sign(L(1), R(0)) (the PE's cross term), from the second L(1) + R(0);
-    // written by the peer's warp w after its sweep once this CTA's warp w has read the
-    // previous terms (cons)
-    float mb[SP ? PL::P : 1][SP ? PL::T : 1];
+    // alpha * min-with-sign(L(1), R(0)) (the PE's cross term), from the second L(1) + R(0)
+    float mb[SP ? 2 : 1][SP ? PL::P : 1][SP ? PL::T : 1];
     uint32_t gx[SP ? 2 : 1][SP ? PL::NW : 1];     // G-check words from the peer (first CTA: t1; second: t0 ^ x_hat0)
     int pst[2][4];                                 // the peer's frontier (global), completion stage, mismatch of its half
     long long pfin[3];                             // frame end (from the second CTA): bit errors, PEs, events
-    int cons[SP ? PL::NWARP : 1];                  // the peer's warps: last sweep whose mailbox terms they read
+    uint32_t tu[SP ? PL::NW : 1];                  // own transformed pinned hard output
     unsigned long long post;                       // second CTA: the first CTA's post (seq << 32 | frontier << 16 | code)
     unsigned long long postv;                      // its broadcast copy
 };
@@ -907,16 +901,10 @@ struct Dec {
     __device__ __forceinline__ void push_x(const float* v) const {
         float r[P];
         own_r0(r);
-        if (it > 0) {  // the peer's warp read the terms of this sweep (sweep 1's push: the frame barriers order it)
-            if (lane == 0)
-                while ((int)ld_volatile(reinterpret_cast<const uint32_t*>(&sm->cons[warp])) < it) {
-                }
-            __syncwarp();
-        }
 #pragma unroll
         for (int j = 0; j < P; ++j) {
             const float x = rank == 0 ? __fmul_rn(alpha, xsmin(v[j], r[j])) : __fadd_rn(v[j], r[j]);
-            st_peer(peer_addr(&sm->mb[j][tid]), x);
+            st_peer(peer_addr(&sm->mb[it & 1][j][tid]), x);
         }
     }
 
@@ -975,7 +963,7 @@ struct Dec {
         for (int j = 0; j < P; ++j) {
             // the first CTA: l_top and R(1) of the top rows from the peer's L(1) + R(0)
             // (sum_bot); the second: l_bot and R(1) of the bottom rows from the cross term
-            const float pm = sm->mb[j][tid];
+            const float pm = sm->mb[(it - 1) & 1][j][tid];
             float rn, x;
             if (rank == 0) {
                 const float l_top = __fmul_rn(alpha, xsmin(lo[j], pm));
@@ -990,8 +978,6 @@ struct Dec {
             const uint32_t w = __ballot_sync(kFull, x < 0.f);
             if (lane == 0) sm->xh[row<0>(j) >> 5] = w;
         }
-        // this warp read its terms (the ballots above consumed them): the peer's warp may refill them
-        if (lane == 0) st_peer(peer_addr(&sm->cons[warp]), it);
         if (rank == 0) act += P;
     }
 
@@ -1264,7 +1250,6 @@ struct Dec {
         for (;;) {
             // the previous frame is done in both CTAs: reset what the peer writes
             if (rank == 1 && tid == 0) sm->post = 0u;
-            if (tid < PL::NWARP) sm->cons[tid] = 0;
             cluster_sync();
             if (rank == 0 && tid == 0) {
                 const unsigned long long idx = atomicAdd(args.queue, 1ull);
@@ -1366,14 +1351,14 @@ struct Dec {
                 // x = the frame's transform: first half t0 ^ t1, second half t1;
                 // the first CTA sends t0 ^ x_hat0, the second t1 and whether its
                 // half mismatches (t1 != x_hat1): both then decide the same
-                // (the thread holding word w, r0 = 32 w, keeps it for the decision)
+                if ((r0 & 31) == 0) sm->tu[r0 >> 5] = word;
+                __syncthreads();
                 const int gs = it & 1;
-                const bool wown = (r0 & 31) == 0;
-                const int wi = r0 >> 5;
                 bool mm1 = false;
-                if (wown) {
-                    st_peer(peer_addr(&sm->gx[gs][wi]), rank == 0 ? word ^ sm->xh[wi] : word);
-                    mm1 = rank == 1 && word != sm->xh[wi];
+                if (tid < NW) {
+                    const uint32_t t = sm->tu[tid];
+                    st_peer(peer_addr(&sm->gx[gs][tid]), rank == 0 ? t ^ sm->xh[tid] : t);
+                    mm1 = rank == 1 && t != sm->xh[tid];
                 }
                 mm1 = __syncthreads_or(mm1);
                 if (tid == 0) {
@@ -1390,9 +1375,9 @@ struct Dec {
                 gfr = max(gfr, pg);
                 if (gfr < N2) {
                     bool mm = false;
-                    if (wown) {
-                        const uint32_t g = sm->gx[gs][wi];
-                        mm = rank == 0 ? ((word ^ g) != sm->xh[wi]) : ((g ^ word) != 0u);
+                    if (tid < NW) {
+                        const uint32_t g = sm->gx[gs][tid];
+                        mm = rank == 0 ? ((sm->tu[tid] ^ g) != sm->xh[tid]) : ((g ^ sm->tu[tid]) != 0u);
                     }
                     converged = !__syncthreads_or(mm || mm1);
                 }
