@@ -36,8 +36,8 @@ def _functions(sass):
 def test_decoder_kernels_have_no_fused_multiply_add():
     fns = _functions(_sass())
     dec = {k: v for k, v in fns.items()
-           if "bp_warp_kernel" in k or "bp_generic_kernel" in k or "bp_cta_kernel" in k}
-    assert len(dec) >= 13 and any("bp_cta_kernel" in k for k in dec)
+           if "bp_warp_kernel" in k or "bp_generic_kernel" in k or "bp_cta_kernel" in k or "bp_pair_kernel" in k}
+    assert len(dec) >= 13 and any("bp_cta_kernel" in k for k in dec) and any("bp_pair_kernel" in k for k in dec)
     for name, lines in dec.items():
         for ln in lines:
             m = re.search(r"\bFFMA2?\b[^;]*;", ln)
@@ -53,3 +53,18 @@ def test_fast_kernel_uses_packed_fp32_and_xorsign_min():
     text = "\n".join(k)
     assert "FADD2" in text and "FFMA2" in text
     assert re.search(r"FMNMX[^;]*XORSIGN", text) or "FMNMX" in text
+
+
+@pytest.mark.skipif(not os.path.exists(CUOBJDUMP), reason="cuobjdump absent")
+def test_pair_kernel_uses_cluster_barrier_and_tmem():
+    """The n = 16384 cluster kernel synchronises the pair with the cluster barrier
+    (barrier.cluster -> UCGABAR_ARV / UCGABAR_WAIT; its DSMEM stores are generic
+    ST.E to cluster-window addresses) and keeps its inner levels, R(0) and L(1) in
+    tensor memory (STTM / LDTM)."""
+    fns = _functions(_sass())
+    k = [v for n, v in fns.items() if "bp_pair_kernelILi13ELi2E" in n]
+    assert k, "bp_pair_kernel<13, 2> missing"
+    text = "\n".join(k[0])
+    assert "UCGABAR_ARV" in text and "UCGABAR_WAIT" in text
+    assert "STTM" in text and "LDTM" in text
+    assert re.search(r"\bST\.E\b", text)
