@@ -107,3 +107,56 @@ def test_decode_count_batches_one_launch_per_sweep(ctx, n):
         P._check(P.lib.pbp_decode_count_batches_device(ctx.handle, C.byref(cs), 2, P._abi.f32p(d_llr.data_ptr()),
                                                        P._abi.u32p(d_u.data_ptr()), frames, 0, 0.9375, 40,
                                                        P._abi.i64p(cnt.data_ptr()), None))
+
+
+def _gloo_gpu_worker(rank, world, port, q):
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    import paper_1505_04979_b200 as P
+    from paper_1505_04979_b200 import dist as D
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pctx = P.Context(0)  # one GPU on the test box: both ranks decode their shards on it
+
+    def gpu_point(code, decoder, seed, first, count, ebn0, alpha, max_iter):
+        return P.simulate_point(code, decoder, seed, first, count, ebn0, alpha, max_iter, ctx=pctx)
+
+    out = []
+    for n, frames, snrs in ((1024, 2001, [2.0, 3.5]), (16384, 151, [2.5])):
+        code = P.PolarCode.construct(n, n // 2, Z0)
+        out.append(D.simulate_sweep_sharded(code, "csfg", 5, frames, snrs, rank=rank, world=world,
+                                            point_fn=gpu_point))
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600, method="thread")
+def test_gloo_world2_gpu_shards_equal_single_process():
+    """dist.simulate_sweep_sharded with the GPU decoder per rank (gloo world of 2; the
+    counters all-reduced on the host): the sums equal one process decoding every trial,
+    at n = 1024 (warp kernel) and n = 16384 (2-CTA cluster kernel)."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mctx = mp.get_context("spawn")
+    q = mctx.Queue()
+    procs = [mctx.Process(target=_gloo_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=500) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1]
+    ctx = P.Context(0)
+    for (n, frames, snrs), got in zip(((1024, 2001, [2.0, 3.5]), (16384, 151, [2.5])), res[0]):
+        code = P.PolarCode.construct(n, n // 2, Z0)
+        whole = [P.simulate_point(code, "csfg", 5, 0, frames, snr, ctx=ctx) for snr in snrs]
+        assert got == whole, n
