@@ -62,7 +62,7 @@ struct Cfg<11> {  // 128 threads x 16 rows, 3 CTAs per SM: four levels in regist
     static constexpr int where(int s) { return s == 11 ? kBits : (s <= 3 || s == 5) ? kReg : kSmem; }
 };
 template <>
-struct Cfg<12> {  // 256 x 16, two frames per SM, every level on chip: four in registers, two in shared memory, five in TMEM
+struct Cfg<12> {  // 256 x 16, two frames per SM, every level on chip: three in registers, two in shared memory, six in TMEM
     static constexpr int LOGT = 8, K = 4, MINB = 2;
     // rx2: the pass-boundary R exchange double-buffered (no barrier before its
     // stores; measured +0.6 % csfg at n = 4096, +2.5 % at n = 8192)
@@ -73,9 +73,9 @@ struct Cfg<12> {  // 256 x 16, two frames per SM, every level on chip: four in r
     static constexpr int TMEM_COLS = 256;
     static constexpr bool TPROT_REG = false;
     static constexpr bool PACK(int kind) { return kind != 2; }
-    static constexpr int where(int s) {
-        return s == 12 ? kBits : (s <= 3 || s == 5) ? kReg : (s == 4 || s == 8) ? kSmem : kTmem;
-    }
+    // level 5 in TMEM too (16 registers freed: +1.8 % csfg, +3.6 % G-stop over registers)
+    // (level 3 in TMEM as well measured 1.4 % slower here)
+    static constexpr int where(int s) { return s == 12 ? kBits : (s <= 3) ? kReg : (s == 4 || s == 8) ? kSmem : kTmem; }
 };
 #if 0  // round-1 layout (two levels in L2)
 template <>
@@ -91,7 +91,7 @@ struct Cfg<12> {  // 256 x 16, two frames per SM: four levels in registers, five
 };
 #endif
 template <>
-struct Cfg<13> {  // 512 x 16: three levels in registers, three in shared memory, six in TMEM (all on chip)
+struct Cfg<13> {  // 512 x 16: two levels in registers, three in shared memory, seven in TMEM (all on chip)
     static constexpr int LOGT = 9, K = 4, MINB = 1;
     // rx2: the pass-boundary R exchange double-buffered (no barrier before its
     // stores; measured +0.6 % csfg at n = 4096, +2.5 % at n = 8192)
@@ -99,8 +99,9 @@ struct Cfg<13> {  // 512 x 16: three levels in registers, three in shared memory
     static constexpr int TMEM_COLS = 512;  // 16 warps: 128 columns of its lane quarter per warp
     static constexpr bool TPROT_REG = false;
     static constexpr bool PACK(int) { return true; }
-    // the inner levels of passes 1 and 2 in TMEM (5 and 6 in shared memory measured 1.8 % slower)
-    static constexpr int where(int s) { return s == 13 ? kBits : (s <= 3) ? kReg : (s % 4 == 0) ? kSmem : kTmem; }
+    // every inner level from 3 on in TMEM (5 and 6 in shared memory measured 1.8 % slower,
+    // level 3 in registers 2.4 % slower)
+    static constexpr int where(int s) { return s == 13 ? kBits : (s <= 2) ? kReg : (s % 4 == 0) ? kSmem : kTmem; }
 };
 template <>
 struct Cfg<14> {  // 1024 x 16: one level in shared memory, four in TMEM, the rest in L2
