@@ -700,10 +700,14 @@ int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
     // Chunks round-robin over the slots' streams: the host->device copy of one
     // chunk overlaps the decode of the others (and a decode's tail overlaps
     // the next chunk's launch).
-    // Chunk sizes double from 4096 frames up to 2^17 and halve again towards
-    // the end: a chunk's copy (PCIe is ~2x faster than the decode) hides
-    // under the previous chunk's decode, and the last kernel's tail is short.
-    constexpr long long kChunkMin = 16384, kEdge = 4096, kCap = 1 << 17;
+    // Chunk sizes double from 16 MB of LLRs (4096 frames at n = 1024) up to
+    // 512 MB and halve again towards the end: a chunk's copy (PCIe is ~2x
+    // faster than the decode) hides under the previous chunk's decode, and the
+    // last kernel's tail is short. Sized in bytes: at n = 16384 one 16384-frame
+    // call is 1 GB, which as a single chunk left its whole upload exposed.
+    const long long fscale = std::max(1, n / 1024);
+    const long long kChunkMin = std::max(64ll, 16384 / fscale), kEdge = std::max(16ll, 4096 / fscale),
+                    kCap = std::max(256ll, (1ll << 17) / fscale);
     std::vector<long long> bounds{0};
     if (frames >= 2 * kChunkMin) {
         std::vector<long long> head, tail;
