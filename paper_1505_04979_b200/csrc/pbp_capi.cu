@@ -700,11 +700,16 @@ int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
     // Chunks round-robin over the slots' streams: the host->device copy of one
     // chunk overlaps the decode of the others (and a decode's tail overlaps
     // the next chunk's launch).
-    // Chunk sizes double from 16 MB of LLRs (4096 frames at n = 1024) up to
-    // 512 MB and halve again towards the end: a chunk's copy (PCIe is ~2x
-    // faster than the decode) hides under the previous chunk's decode, and the
-    // last kernel's tail is short. Sized in bytes: at n = 16384 one 16384-frame
-    // call is 1 GB, which as a single chunk left its whole upload exposed.
+    // Chunk sizes grow by 1.3x from 16 MB of LLRs (4096 frames at n = 1024)
+    // up to 512 MB and shrink again towards the end, so the last kernel's tail
+    // is short. The copies run back to back on the copy engine, so chunk c's
+    // data arrives when the copies of chunks 1..c are done; the decoder never
+    // waits while each chunk is at most (decode time / copy time - 1) of all
+    // chunks before it: with PCIe only ~1.3x faster than the n = 1024 csfg
+    // decode, doubling chunks starved the decoder for ~6 ms per 700k frames
+    // (tools/e2e_probe.py: 75.0 vs 67.8 ms device at 3 dB). Sized in bytes:
+    // at n = 16384 one 16384-frame call is 1 GB, which as a single chunk left
+    // its whole upload exposed.
     const long long fscale = std::max(1, n / 1024);
     const long long kChunkMin = std::max(64ll, 16384 / fscale), kEdge = std::max(16ll, 4096 / fscale),
                     kCap = std::max(256ll, (1ll << 17) / fscale);
@@ -720,7 +725,7 @@ int pbp_decode_batch(pbp_ctx* ctx, const pbp_code* code, int decoder, const floa
             const long long b = std::min(sz, rem);
             tail.push_back(b);
             rem -= b;
-            sz = std::min(sz * 2, kCap);
+            sz = std::min(sz * 13 / 10, kCap);
         }
         for (long long v : head) bounds.push_back(bounds.back() + v);
         for (auto it = tail.rbegin(); it != tail.rend(); ++it) bounds.push_back(bounds.back() + *it);
