@@ -34,6 +34,22 @@
 // fma(alpha, m, +0) so R is never -0); frames with |LLR| beyond the
 // clamp-free bound or non-finite are re-routed to the generic kernel, which
 // keeps every clamp.
+//
+// Levels that the register file cannot hold live in tensor memory where the
+// layout allocates it (thread-private levels: one tcgen05.ld/st of P columns
+// per stage): n = 4096 at two CTAs per SM (256 columns each; the occupancy
+// API reports one CTA per SM for a TMEM kernel, but CTAs whose columns fit the
+// SM's 512 co-reside), n = 8192 and 16384 at one. R(0) stays in TMEM where a
+// column slot is free.
+//
+// n = 16384 csfg runs as a 2-CTA thread-block cluster per frame (SP = true,
+// bp_pair_kernel): each CTA holds half of the frame in the n = 8192 layout on
+// its own SM, so every level is on chip; only the frame's stage 0 couples the
+// halves (row r of both halves at the same thread of both CTAs: one term per
+// row through distributed shared memory per sweep), the half holding the
+// frontier checks the candidates (the first CTA posts its frontier to the
+// second), and the pinned G-check splits along the transform's top level with
+// one cluster barrier per iteration.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
