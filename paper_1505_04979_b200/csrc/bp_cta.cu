@@ -51,6 +51,7 @@
 // second), and the pinned G-check splits along the transform's top level with
 // one cluster barrier per iteration.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -1558,7 +1559,12 @@ static cudaError_t launch_pair(const DecodeArgs& a, cudaStream_t st) {
     cfg.stream = st;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    static int max_clusters = 0;  // per process (one device model)
+    // resident clusters per device, cached (host threads of pbp_simulate_sweep_multi launch concurrently)
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    int max_clusters = dev < 64 ? cache[dev].load(std::memory_order_relaxed) : 0;
     if (!max_clusters) {
         cfg.gridDim = dim3(2 * 148 * 4);
         int nc = 0;
@@ -1566,6 +1572,7 @@ static cudaError_t launch_pair(const DecodeArgs& a, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         if (nc < 1) return cudaErrorInvalidConfiguration;
         max_clusters = nc;
+        if (dev < 64) cache[dev].store(nc, std::memory_order_relaxed);
         if (getenv("PBP_PAIR_INFO")) fprintf(stderr, "pbp: bp_pair_kernel %zu B shared/CTA, %d resident clusters\n", smem, nc);
     }
     long long ncl = std::min<long long>(max_clusters, a.frames);
