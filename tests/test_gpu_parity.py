@@ -584,3 +584,24 @@ def test_cta_kernel_special_llr_values(ctx, n):
         assert np.array_equal(P.unpack_bits(got["u_hat_bits"], n), exp["u_hat"]), kind
         for f in ("iterations", "pe", "stop", "n_events"):
             assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), (kind, f)
+
+
+@pytest.mark.parametrize("n,frames", [(4096, 9000), (16384, 2600)])
+def test_chunked_batch_large_codes(ctx, n, frames):
+    """At n >= 2048 the host pipeline's chunks are sized in bytes (16 MB of LLRs
+    first, growing 1.3x): a multi-chunk call on the CTA kernel (n = 4096) and on the
+    2-CTA cluster kernel (n = 16384), with re-routed frames in several chunks, equals
+    one launch per part."""
+    code = P.PolarCode.construct(n, n // 2, Z0)
+    llr, _, _ = P.generate(code, 5, 0, frames, 4.0, ctx=ctx)
+    big = [3, frames // 3, frames - 2]
+    llr[big, 11] = 1e30
+    whole = P.decode_batch(code, "csfg", llr, 0.9375, 40, ctx=ctx)
+    launches, rerouted = ctx.last_launch_info()
+    assert rerouted == len(big) and launches >= 4, (launches, rerouted)
+    step = frames // 4
+    for a in range(0, frames, step):
+        b = min(frames, a + step)
+        part = P.decode_batch(code, "csfg", llr[a:b], 0.9375, 40, ctx=ctx)
+        for f in whole:
+            assert np.array_equal(whole[f][a:b], part[f]), (f, a)
