@@ -15,8 +15,8 @@ Z0 = math.exp(-0.5)
 LIB = O.REF or O.C
 
 
-@pytest.mark.parametrize("n,generic", [(1024, False), (4096, False), (1024, True)],
-                         ids=["warp", "cta", "generic"])
+@pytest.mark.parametrize("n,generic", [(1024, False), (4096, False), (16384, False), (1024, True)],
+                         ids=["warp", "cta", "cluster", "generic"])
 def test_simulate_batches_per_batch_counters(ctx, n, generic):
     code = P.PolarCode.construct(n, n // 2, Z0)
     frames = 1000 if n == 1024 else 600
