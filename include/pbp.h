@@ -235,11 +235,11 @@ int pbp_simulate_sweep_multi(const int* devices, int ndev, const pbp_code* code,
  * 0 = the generic kernel only. For tests and bench introspection. */
 int pbp_kernel_path(int32_t n);
 /* CTAs per frame of the fast kernel for (n, decoder): 2 = the frame split
- * over a 2-CTA thread-block cluster (n = 16384 csfg: each CTA holds half of
- * the frame on its SM, the frame's stage 0 exchanged through distributed
- * shared memory; environment PBP_PAIR=0 selects one CTA per frame), 1 = one
- * CTA (or warp) per frame, 0 = no fast kernel for n. Freeze-event traces
- * always decode one frame per CTA. */
+ * over a 2-CTA thread-block cluster (n = 16384, every decoder: each CTA holds
+ * half of the frame on its SM, the frame's stage 0 exchanged through
+ * distributed shared memory; environment PBP_PAIR=0 selects one CTA per
+ * frame), 1 = one CTA (or warp) per frame, 0 = no fast kernel for n.
+ * Freeze-event traces always decode one frame per CTA. */
 int pbp_kernel_cluster(int32_t n, int decoder);
 /* Route every decode of this context through the generic kernel (on != 0).
  * Test hook: lets the suite check both kernels against the oracle. */

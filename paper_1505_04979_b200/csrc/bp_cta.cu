@@ -1244,7 +1244,8 @@ struct Dec {
         }
     }
 
-    // SP: one half of each frame of length 2N on a 2-CTA cluster (csfg).
+    // SP: one half of each frame of length 2N on a 2-CTA cluster (csfg; G-stop and
+    // fixed-iteration decodes run the same loop without the frontier).
     // Per iteration: the cross stage (the frame's stage 0) from the peer's
     // L(1) in the mailbox, the check of the frame's stage-0 candidate by the
     // half holding the frontier, the local sweep (the frame's stages 1..m-1,
@@ -1357,8 +1358,12 @@ struct Dec {
                     if constexpr (PL::NTM > 0) fixup_tmem();
                 }
                 push_l1();
+                if constexpr (KIND == 0) {  // fixed iterations: no G-check, only the exchange's ordering
+                    cluster_sync();
+                    continue;
+                }
                 // pinned G-check inputs: this half's hard output (rows < frontier
-                // from decided_u), transformed over the half's row bits
+                // from decided_u; G-stop: frontier 0), transformed over the half's row bits
                 uint32_t g = bits_transform<K>(u_group(frontier));
                 g = lane_transform<5>(g);
                 g = warp_transform<PL::LOGT - 5>(g);
@@ -1626,8 +1631,8 @@ long long cta_scratch_floats(int m) {
 bool cta_pair_on(int m, int kind) {
     const char* e = getenv("PBP_PAIR");  // read per launch: tests compare both layouts in one process
     const int v = e ? atoi(e) : 1;
-    // n = 4096 on pairs only as an experiment (PBP_PAIR=2): slower, see DESIGN.md section 5
-    return kind == 2 && ((v && m == 14) || (v >= 2 && m == 12));
+    // n = 4096 on pairs only as an experiment (PBP_PAIR=2, csfg): slower, see DESIGN.md section 5
+    return (v && m == 14 && kind >= 0 && kind <= 2) || (v >= 2 && m == 12 && kind == 2);
 }
 static bool cta_pair(const DecodeArgs& a) { return cta_pair_on(a.m, a.kind) && !a.events && !a.ev_xhat; }
 template <int M>
@@ -1645,7 +1650,11 @@ int cta_pair_warps_per_sm(int m) {
 size_t cta_pair_smem_bytes(int m) { return m == 12 ? sizeof(cta::Smem<11, true>) : sizeof(cta::Smem<13, true>); }
 
 cudaError_t launch_cta(const DecodeArgs& a, int grid, cudaStream_t st) {
-    if (cta_pair(a)) return a.m == 14 ? cta::launch_pair<13, 2>(a, st) : cta::launch_pair<11, 2>(a, st);
+    if (cta_pair(a)) {
+        if (a.m == 12) return cta::launch_pair<11, 2>(a, st);
+        return a.kind == 0 ? cta::launch_pair<13, 0>(a, st)
+                           : (a.kind == 1 ? cta::launch_pair<13, 1>(a, st) : cta::launch_pair<13, 2>(a, st));
+    }
     switch (a.m) {
         case 11: return cta::launch_m<11>(a, grid, st);
         case 12: return cta::launch_m<12>(a, grid, st);

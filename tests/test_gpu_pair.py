@@ -41,8 +41,8 @@ def _same_gpu(a, b, tag):
 @pytest.fixture
 def pair(monkeypatch):
     monkeypatch.setenv("PBP_PAIR", "1")
-    assert P.lib.pbp_kernel_cluster(N, 2) == 2
-    assert P.lib.pbp_kernel_cluster(N, 1) == 1 and P.lib.pbp_kernel_cluster(8192, 2) == 1
+    assert P.lib.pbp_kernel_cluster(N, 2) == 2 and P.lib.pbp_kernel_cluster(N, 1) == 2
+    assert P.lib.pbp_kernel_cluster(N, 0) == 2 and P.lib.pbp_kernel_cluster(8192, 2) == 1
 
 
 def _oracle(fz, llr, max_iter):
@@ -176,3 +176,24 @@ def test_pair_n4096_experiment(ctx, monkeypatch, snr):
     assert np.array_equal(u, exp["u_hat"])
     for f in ("iterations", "pe", "stop", "n_events"):
         assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), f
+
+
+@pytest.mark.parametrize("kind", ["baseline", "gmatrix"])
+def test_pair_gstop_and_fixed_iterations(ctx, pair, monkeypatch, kind):
+    """G-stop and fixed-iteration decodes at n = 16384 on the cluster kernel: against
+    the oracle on channel frames (2.5-6 dB: some frames stop on the G-check) and
+    identical to one CTA per frame on 1000 device-generated frames."""
+    fz = O.construct(N, N // 2, Z0)
+    for snr in (2.5, 4.0, 6.0):
+        _, llr64 = O.trials(5, 0, 4, fz, snr, lib=O.C)
+        llr = llr64.astype(np.float32)
+        exp = O.decode_batch(kind, fz, llr, 0.9375, 20, prec=32)
+        got = P.decode_batch(_code(fz), kind, llr, 0.9375, 20, ctx=ctx)
+        _same(got, exp, f"{kind} {snr} dB")
+    code = P.PolarCode.construct(N, N // 2, Z0)
+    llr, _, _ = P.generate(code, 5, 0, 1000, 4.5, ctx=ctx)
+    runs = []
+    for on in ("1", "0"):
+        monkeypatch.setenv("PBP_PAIR", on)
+        runs.append(P.decode_batch(code, kind, llr, 0.9375, 40, ctx=ctx))
+    _same_gpu(runs[0], runs[1], kind)
