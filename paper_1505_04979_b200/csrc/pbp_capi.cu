@@ -327,8 +327,6 @@ int run_decode(pbp_ctx* ctx, const DecodeReq& r, DecodeSlot& s, cudaStream_t st)
         const int per_sm = warp_occupancy(ctx, r.kind);
         long long grid = std::min<long long>((long long)per_sm * ctx->sm_count, r.frames);
         if (const char* gc = getenv("PBP_GRID_CAP")) grid = std::max(1ll, std::min(grid, atoll(gc)));  // experiments
-        if (const char* gf = getenv("PBP_GRID_FORCE"))  // experiments (kernels without L2 scratch only)
-            grid = std::max(1ll, std::min(r.frames, atoll(gf)));
         cudaError_t e;
         if (fk == 1) {
             a.r0s = s.r0s.p;
